@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark: effective HBM GB/s and ms/iter of the indirect-increment loop,
+hierarchical vs global colouring, on 1..8 B200s.
+
+    python bench.py [--gpus N --steps K --warmup W --config C5 --reorder gps]
+    python bench.py --impl reference        # the reference's CPU loop, same metric
+
+Default workload (BASELINE.json configs[4], the 1/2/4/8-GPU config): the
+Airfoil-style edge->cell flux loop on a 5657 x 5657 quad mesh (63,991,984
+edges, 32,001,649 cells, fp64), hierarchical two-layer colouring (GPS
+blocks, block size 128, dataflow schedule), values on the 1/1024 grid from
+a counter hash (synthetic).  One step = one full execution of the loop over
+the mesh.  Effective GB/s uses the paper's formula (simulator.py:315-328):
+each array once, the incremented array twice, 4-byte mapping entries.
+With N>1 GPUs the mesh is decomposed into x-slabs (owner compute, NCCL halo
+exchange of q and of increments); `value` is the whole-mesh bytes over the
+max-over-ranks step time (strong scaling: the mesh is fixed).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+CONFIGS = {
+    # name: (family, dims, kernel, dtype, staging)
+    "C1": ("quad2d", (848, 848), "flux", "f64", "all-indirect"),
+    "C2": ("tri2d", (1095, 1095), "flux", "f32", "all-indirect"),
+    "C3": ("hex3d-nodes", (160, 160, 160), "scatter8", "f64", "all-indirect"),
+    "C4": ("hex3d-faces", (200, 200, 200), "face-flux", "f64", "increment-only"),
+    "C5": ("quad2d", (5657, 5657), "flux", "f64", "all-indirect"),
+}
+METRIC = "effective HBM GB/s and ms/iter per indirect loop vs global colouring, 1/2/4/8 GPU"
+L2_BYTES = 126 * 2**20
+
+
+def peaks():
+    try:
+        return json.loads((REPO / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def hbm_peak():
+    p = peaks()
+    if "hbm_gbs" in p:
+        return float(p["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------------
+# clocks
+# ----------------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.rows = []
+        self.proc = None
+        self.dev = device_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8 for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------
+# workload
+# ----------------------------------------------------------------------------------
+
+
+def quad_mesh(nx, ny, seed=0, xlo=0, xhi=None):
+    """Full (or x-slab) quad mesh with hashed 1/1024-grid values (synthetic)."""
+    import torch
+
+    import paper_1802_03749_b200 as mp
+    from paper_1802_03749_b200.workloads import hashed_grid_values, quad2d_table
+
+    table, gids = quad2d_table(nx, ny, xlo, xhi)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    cells_used = np.unique(table) if (xlo != 0 or (xhi is not None and xhi != nx)) else None
+    ncell = nx * ny
+    if cells_used is None:
+        cid = torch.arange(ncell, dtype=torch.int64, device=dev)
+        local_table = table
+    else:
+        cid = torch.as_tensor(cells_used, device=dev)
+        local_table = np.searchsorted(cells_used, table)
+    q = hashed_grid_values(cid[:, None] * 4 + torch.arange(4, device=dev), seed, 1).cpu().numpy()
+    g = torch.as_tensor(gids, device=dev)
+    w = hashed_grid_values(g[:, None] * 2 + torch.arange(2, device=dev), seed, 3).cpu().numpy()
+    edges = mp.MeshSet("edges", local_table.shape[0])
+    cells = mp.MeshSet("cells", cid.numel())
+    data = [mp.DataArray("q", cells, 4, q.reshape(-1)), mp.DataArray("res", cells, 4, np.zeros(cid.numel() * 4)),
+            mp.DataArray("w", edges, 2, w.reshape(-1))]
+    mesh = mp.Mesh.build([edges, cells], [mp.Mapping("e2c", edges, cells, local_table)], data,
+                         {"family": "quad2d", "dims": f"{nx} {ny}", "seed": str(seed), "dtype": "f64"})
+    return mesh, (None if cells_used is None else cells_used)
+
+
+def make_mesh(cfg_name, seed=0):
+    import paper_1802_03749_b200 as mp
+    from paper_1802_03749_b200 import workloads
+
+    family, dims, kname, dtype, staging = CONFIGS[cfg_name]
+    if family == "quad2d":
+        mesh, _ = quad_mesh(*dims, seed=seed)
+    else:
+        mesh = workloads.generate_mesh(family, dims, seed=seed, dtype=dtype, arrays=workloads.arrays_for_kernel(kname))
+    return mesh, mp.kernel_for_mesh(kname, mesh), staging
+
+
+# ----------------------------------------------------------------------------------
+# timing
+# ----------------------------------------------------------------------------------
+
+
+class L2Flusher:
+    def __init__(self, needed):
+        import torch
+
+        self.buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda") if needed else None
+
+    def __call__(self):
+        if self.buf is not None:
+            self.buf.add_(1)
+
+
+def time_steps(step, K, W, flush, stream=None):
+    """Per-step CUDA-event times (ms) on the launching stream, L2 flushed
+    between steps when the working set fits in L2."""
+    import torch
+
+    for _ in range(W):
+        flush()
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for a, b in evs:
+        flush()
+        a.record()
+        step()
+        b.record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def kernel_share(step, K):
+    """Average device duration of the launches inside one step (CUDA events
+    around the hot kernel launches only); for the dataflow schedule this is
+    the single executor kernel."""
+    import torch
+
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(K):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / K
+
+
+def cpu_baseline(mesh, kernel_name, seconds=10.0, max_edges=4_000_000):
+    """The reference CPU loop (oracle restatement of execute_serial,
+    simulator.py:215-242; numpy, single-threaded) on a bounded sample."""
+    from oracle import loops
+
+    m = next(iter(mesh.mappings.values()))
+    n = min(m.from_set.size, max_edges)
+    table = m.table[:n]
+    used = np.unique(table)
+    local = np.searchsorted(used, table)
+    read = {"flux": "q", "face-flux": "state", "face-flux-heavy": "state"}.get(kernel_name)
+    direct = {"flux": "w", "flux-noread": "w", "scatter8": "stress"}.get(kernel_name, "facew")
+    inc = {"flux": "res", "flux-noread": "res", "scatter8": "force"}.get(kernel_name, "flux")
+    ind = None if read is None else np.ascontiguousarray(mesh.data[read].view2d()[used])
+    d = np.ascontiguousarray(mesh.data[direct].view2d()[:n])
+    r0 = np.ascontiguousarray(mesh.data[inc].view2d()[used])
+    arrays = [(used.size, r0.shape[1], r0.itemsize, True), (n, d.shape[1], d.itemsize, False)]
+    if ind is not None:
+        arrays.append((used.size, ind.shape[1], ind.itemsize, False))
+    ub = loops.useful_bytes(n, m.arity, arrays)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        loops.serial_loop(kernel_name, local, ind, d, r0)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": round(ub / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"execute_serial restated in numpy (oracle/loops.py) on the first {n} of "
+                      f"{m.from_set.size} elements ({used.size} points), median of {len(times)} runs, "
+                      f"{t * 1e3:.1f} ms/run",
+            "ms_per_run": round(t * 1e3, 3), "useful_bytes": ub}
+
+
+# ----------------------------------------------------------------------------------
+# arms
+# ----------------------------------------------------------------------------------
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    mesh, kernel, _ = make_mesh(args.config)
+    family, dims, kname, dtype, _ = CONFIGS[args.config]
+    # warmup W, then K timed steps of the bounded sample
+    base = cpu_baseline(mesh, kname, seconds=0.0)
+    per_step = []
+    for i in range(args.warmup + args.steps):
+        b = cpu_baseline(mesh, kname, seconds=0.0)
+        if i >= args.warmup:
+            per_step.append(b["ms_per_run"])
+    ms = statistics.median(per_step)
+    val = round(base["useful_bytes"] / (ms * 1e-3) / 1e9, 4)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": f"{args.config} {family} {'x'.join(map(str, dims))} {kname} {dtype} "
+                               "(bounded sample, see cpu_baseline.sample)"},
+        "cpu_baseline": {**{k: base[k] for k in ("unit", "cores", "kind", "sample")}, "value": val},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def our_arm(args):
+    import torch
+
+    import paper_1802_03749_b200 as mp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        from paper_1802_03749_b200 import decomp
+
+        return decomp.bench_rank(args, rank, world)
+    torch.cuda.set_device(0)
+    family, dims, kname, dtype, staging = CONFIGS[args.config]
+    t0 = time.perf_counter()
+    mesh, kernel, staging = make_mesh(args.config)
+    t_gen = time.perf_counter() - t0
+    ub = mp.useful_bytes(kernel, mesh)
+    flush = L2Flusher(ub < 2 * L2_BYTES)
+
+    results = {}
+    plans = {}
+    t0 = time.perf_counter()
+    hier = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(
+        reorder=args.reorder, layout=args.layout, staging=staging, block_size=args.block_size))
+    t_plan_h = time.perf_counter() - t0
+    plans["hier"] = hier
+    sampler = ClockSampler()
+    sampler.start()
+    loops = {}
+    for sched in ("dataflow", "colour"):
+        lp = mp.bind(hier, kernel, schedule=sched)
+        loops[sched] = lp
+        times = time_steps(lp.run, args.steps, args.warmup, flush)
+        results[f"hier_{sched}"] = times
+    clocks = sampler.stop()
+
+    t0 = time.perf_counter()
+    glob = mp.build_global_plan(mesh, kernel, mp.PlanConfig(strategy="global", reorder=args.global_reorder,
+                                                              layout=args.layout, block_size=args.block_size))
+    t_plan_g = time.perf_counter() - t0
+    gl = mp.bind(glob, kernel)
+    results["global"] = time_steps(gl.run, args.steps, args.warmup, flush)
+
+    # end to end through the public API with host buffers (pinned), H2D + D2H in the region
+    main = loops[args.schedule]
+    inputs = {a.array: hier.mesh.data[a.array].values for a in kernel.args}
+    inc_name = next(a.array for a in kernel.args if a.mode == "increment")
+    out = torch.empty(hier.mesh.data[inc_name].values.size, dtype=main.tensors[inc_name].dtype, pin_memory=True)
+    h2d = sum(v.nbytes for v in inputs.values())
+    d2h = out.numel() * out.element_size()
+
+    def e2e_step():
+        main.run_host(inputs, out)
+
+    e2e_times = time_steps(e2e_step, max(3, args.steps // 2), args.warmup, flush)
+
+    ms = statistics.median(results[f"hier_{args.schedule}"])
+    ms_glob = statistics.median(results["global"])
+    ms_col = statistics.median(results["hier_colour"])
+    ms_df = statistics.median(results["hier_dataflow"])
+    gbps = ub / (ms * 1e-3) / 1e9
+    peak, peak_kind = hbm_peak()
+    launches = main.launches_per_run()
+    cpu = cpu_baseline(mesh, kname, seconds=args.cpu_seconds) if args.cpu_seconds > 0 else None
+    traffic = None
+    prof = REPO / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(f"{args.config}:{args.reorder}:{args.schedule}")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": round(gbps, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {
+            "workload": f"{args.config}: {family} {'x'.join(map(str, dims))} {kname} {dtype}, "
+                        f"{mesh.sets[kernel.iter_set_name(mesh)].size} elements",
+            "strategy": "hier", "reorder": args.reorder, "layout": args.layout, "staging": staging,
+            "block_size": args.block_size, "schedule": args.schedule,
+            "l2": "flushed between steps" if flush.buf is not None else "inputs larger than L2 (no flush)",
+            "useful_bytes_per_step": ub, "parallelism": "single GPU",
+        },
+        "vs_global": {
+            "global_ms": round(ms_glob, 5), "global_gbps": round(ub / (ms_glob * 1e-3) / 1e9, 2),
+            "global_reorder": args.global_reorder, "global_colours": glob.num_colours,
+            "hier_colour_schedule_ms": round(ms_col, 5), "hier_dataflow_ms": round(ms_df, 5),
+            "speedup_hier_over_global": round(ms_glob / ms, 3),
+            "block_colours": hier.block_colours.num_colours, "num_blocks": hier.num_blocks,
+            "reuse_factor": round(mp.reuse_factor(hier), 4),
+            "thread_colours_mean": round(float(hier.thread_colour_counts.mean()), 3),
+        },
+        "roofline": {"bound": "hbm", "achieved": round(gbps, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(gbps / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": f"hier_block_kernel ({args.schedule} schedule, {launches} launch/step)"},
+        "e2e": {"value": round(ub / (statistics.median(e2e_times) * 1e-3) / 1e9, 3), "unit": "GB/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": round(statistics.median(e2e_times), 3),
+                "path": "DeviceLoop.run_host: pinned host arrays -> H2D -> executor -> D2H"},
+        "gpu_launches": int(launches * args.steps),
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+        "plan_build_s": {"generate": round(t_gen, 2), "hier": round(t_plan_h, 2), "global": round(t_plan_g, 2)},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
+    ap.add_argument("--reorder", default="gps")
+    ap.add_argument("--global-reorder", default="gps")
+    ap.add_argument("--layout", default="aos")
+    ap.add_argument("--block-size", type=int, default=128)
+    ap.add_argument("--schedule", default="dataflow", choices=("dataflow", "colour"))
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    return our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,197 @@
+/*
+ * meshplan_b200.h -- C ABI of the B200-native indirect-increment engine.
+ *
+ * Plain C: pointers, sizes and PODs only; no torch or C++ types.  Device
+ * pointers are CUDA global-memory addresses owned by the caller; `stream`
+ * is a cudaStream_t passed as void*.  Every entry point returns an mp_status
+ * (0 = ok); the message of the last failure on the calling thread is
+ * available from mp_last_error().  The status values follow the reference
+ * CLI exit codes (pkg/src/meshplan/cli.py:368-377, errors.py:8-29).
+ *
+ * Which reference interface each entry point replaces is noted beside it.
+ * The reference is pure Python (pkg/src/meshplan); its seams are
+ *   Seam A  meshplan._accel  (pkg/src/meshplan/_accel/__init__.py:43-50)
+ *   Seam B  the loop/plan API (plan.py:408, plan.py:467, simulator.py:215/355/525)
+ * INTEGRATION.md shows the ctypes binding a maintainer would add.
+ */
+#ifndef MESHPLAN_B200_H
+#define MESHPLAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t mp_status;
+enum {
+  MP_OK = 0,
+  MP_ERR_CUDA = 1,       /* CUDA runtime failure                          */
+  MP_ERR_KERNEL = 2,     /* KernelSpecError   (exit code 2)               */
+  MP_ERR_RACE = 3,       /* RaceError         (exit code 3)               */
+  MP_ERR_CAPACITY = 4,   /* CapacityError     (exit code 4)               */
+  MP_ERR_FORMAT = 5,     /* FileFormatError   (exit code 5)               */
+  MP_ERR_VALIDATION = 6  /* MeshValidationError (exit code 2)             */
+};
+
+enum { MP_F64 = 0, MP_F32 = 1, MP_I64 = 2, MP_I32 = 3 };          /* element types  */
+enum { MP_AOS = 0, MP_SOA = 1 };                                   /* array layouts  */
+enum {                                                             /* device element ops */
+  MP_OP_FLUX = 0,            /* bench_kernels.py:154-189                   */
+  MP_OP_FLUX_NOREAD = 1,     /* bench_kernels.py:174-176                   */
+  MP_OP_SCATTER8 = 2,        /* bench_kernels.py:192-207                   */
+  MP_OP_FACE_FLUX = 3,       /* bench_kernels.py:210-246                   */
+  MP_OP_FACE_FLUX_HEAVY = 4  /* bench_kernels.py:234-237                   */
+};
+enum { MP_SCHED_COLOUR = 0, MP_SCHED_DATAFLOW = 1 };              /* hierarchical schedules */
+
+/* One indirect loop bound to device arrays (plan numbering).
+ * Indirect arrays (ind_read, inc) use ind_layout; direct arrays are SoA
+ * (plan.py:381-398).  Element e's slot s point is map[e*arity+s] (AoS) or
+ * map[s*n_elems+e] (SoA). */
+typedef struct mp_loop {
+  int32_t op;            /* MP_OP_*                                        */
+  int32_t unit;          /* 1: unit-increment variant (incidence counting)  */
+  int32_t dtype;         /* MP_F64 ... shared by every array of the loop   */
+  int32_t ind_layout;    /* MP_AOS / MP_SOA                                */
+  int64_t n_elems;       /* iteration-set size                             */
+  int64_t n_points;      /* to-set size                                    */
+  int32_t arity;
+  int32_t map_layout;    /* MP_AOS / MP_SOA                                */
+  const int32_t* map;
+  const void* ind_read;  /* q / state, or NULL                             */
+  int32_t ind_read_comps;
+  int32_t dir_comps;
+  const void* dir_read;  /* w / stress / facew (SoA)                       */
+  void* inc;             /* res / force / flux, incremented in place        */
+  int32_t inc_comps;
+  int32_t pad_;
+} mp_loop;
+
+/* Device-resident hierarchical plan (HierarchicalPlan, plan.py:132-185).
+ * Blocks are contiguous element ranges; a point's shared slot is its
+ * position in the block's ascending staged list (plan.py:168-182),
+ * materialised here as local_slots (per element and slot) and
+ * written_slots (per written entry). */
+typedef struct mp_hier_plan {
+  int32_t num_blocks;
+  int32_t block_size;           /* widest block (CTA width)                 */
+  int32_t stage_reads;          /* 1: all-indirect staging, 0: increment-only */
+  int32_t max_staged;           /* widest staged list (shared sizing)        */
+  const int32_t* block_offsets;   /* [nb+1]                                  */
+  const int32_t* staged_offsets;  /* [nb+1]                                  */
+  const int32_t* staged_ids;      /* ascending per block                     */
+  const int32_t* written_offsets; /* [nb+1]                                  */
+  const int32_t* written_ids;     /* ascending per block                     */
+  const uint16_t* written_slots;  /* staged slot of each written entry       */
+  const uint16_t* local_slots;    /* [n_elems*arity] staged slot per map entry */
+  const uint8_t* thread_colours;  /* [n_elems] sorted within each block      */
+  const int32_t* colour_counts;   /* [nb] thread colours per block           */
+  /* MP_SCHED_COLOUR: one launch per block colour */
+  int32_t num_block_colours;
+  int32_t pad_;
+  const int32_t* colour_block_offsets_host; /* host [ncol+1]                  */
+  const int32_t* blocks_by_colour;          /* device [nb], (colour, id) order */
+  /* MP_SCHED_DATAFLOW: one launch, blocks in a topological order of the
+   * lower-colour conflict DAG; each block waits for its predecessors. */
+  const int32_t* order;           /* [nb]                                    */
+  const int32_t* pred_offsets;    /* [nb+1]                                  */
+  const int32_t* preds;           /* conflicting blocks of lower colour      */
+  uint32_t* flags;                /* [nb] epoch stamps, zero-initialised     */
+  uint32_t* tickets;              /* [2] ticket counters, zero-initialised   */
+} mp_hier_plan;
+
+/* ---- library ------------------------------------------------------------ */
+const char* mp_last_error(void);
+const char* mp_version(void);
+int32_t mp_device_sm_count(int32_t device);
+
+/* ---- executors (Seam B) --------------------------------------------------- */
+/* execute_global (simulator.py:355-439): one launch per colour range
+ * [colour_offsets[c], colour_offsets[c+1]) (host array), direct non-atomic
+ * read-modify-write of inc; bit-exact with the reference colour order. */
+mp_status mp_exec_global(const mp_loop* loop, const int64_t* colour_offsets, int32_t num_colours,
+                         int32_t block_size, void* stream);
+
+/* execute_hierarchical (simulator.py:525-656): stage, compute, apply
+ * increments in shared memory one thread colour at a time, scatter the
+ * written list once per block.  `epoch` must increase by one per call on a
+ * plan when schedule == MP_SCHED_DATAFLOW (flags are epoch stamps). */
+mp_status mp_exec_hier(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule, uint32_t epoch,
+                       void* stream);
+
+/* execute_serial (simulator.py:215-230) on the device: per-element
+ * increments to a temp array, then per point an ordered sum over its
+ * (element, slot) references (inverse CSR, mesh.py:251-267), i.e. exactly the
+ * np.add.at order.  temp must hold n_elems*arity*inc_comps elements. */
+mp_status mp_exec_serial(const mp_loop* loop, const int32_t* inv_offsets, const int32_t* inv_refs, void* temp,
+                         void* stream);
+
+/* ---- race checks (simulator.py:245-261, 446-469) ---------------------------- */
+/* Keys (group*key_span + point) over every (element, written point) ref;
+ * returns in first_pair[0..1] the first pair of distinct elements sharing a
+ * key in (key, element) order, or -1/-1.  refs are per-element CSR. */
+mp_status mp_race_check(int64_t n_items, const int64_t* ref_offsets, const int32_t* refs, const int64_t* groups,
+                        int64_t key_span, int64_t* first_pair, void* stream);
+
+/* ---- planner kernels ------------------------------------------------------ */
+/* Per block: ascending unique points referenced through the slots in
+ * slot_mask.  Pass 1 (ids == NULL): counts[b].  Pass 2: fill ids at
+ * offsets[b].  (plan.py:582-603) */
+mp_status mp_plan_block_points(int32_t nb, const int32_t* block_offsets, const int32_t* map, int64_t n_elems,
+                               int32_t arity, int32_t map_layout, uint32_t slot_mask, int32_t max_block,
+                               int32_t* counts, const int32_t* offsets, int32_t* ids, void* stream);
+
+/* local_slots[e*arity+s] = position of map(e,s) in block's ids list (binary
+ * search); written_slots likewise for a second list.  Returns
+ * MP_ERR_CAPACITY when a point is missing (plan.py:168-182). */
+mp_status mp_plan_local_slots(int32_t nb, const int32_t* block_offsets, const int32_t* map, int64_t n_elems,
+                              int32_t arity, int32_t map_layout, uint32_t slot_mask, const int32_t* staged_offsets,
+                              const int32_t* staged_ids, uint16_t* local_slots, const int32_t* written_offsets,
+                              const int32_t* written_ids, uint16_t* written_slots, void* stream);
+
+/* Per-block thread colouring (plan.py:260-284): conflict graph of elements
+ * sharing a written point, smallest-last order (numpy_impl.py:95-111,
+ * key deg*(k+1)+u), first-fit greedy (numpy_impl.py:62-92).  Outputs the
+ * unsorted colour of each element, the colour count per block, and the
+ * stable colour sort as local order (plan.py:508-517). */
+mp_status mp_plan_thread_colours(int32_t nb, const int32_t* block_offsets, const int32_t* map, int64_t n_elems,
+                                 int32_t arity, int32_t map_layout, uint32_t written_mask, int32_t max_block,
+                                 int32_t* colours, int32_t* counts, int32_t* sorted_order, void* stream);
+
+/* Sequential greedy colouring of items over shared points, host C++,
+ * bit-identical to greedy_colour_csr (numpy_impl.py:12-60). */
+mp_status mp_greedy_colour_csr(int64_t n_items, const int64_t* indptr, const int64_t* indices, int64_t n_points,
+                               int32_t least_loaded, int64_t* colours);
+
+/* First-fit / least-loaded greedy over an adjacency CSR in a given order
+ * (numpy_impl.py:62-92), host C++. */
+mp_status mp_greedy_colour_adj(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* order,
+                               int32_t least_loaded, int64_t* colours);
+
+/* Smallest-last elimination order (numpy_impl.py:95-111), host C++. */
+mp_status mp_smallest_last_order(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* order);
+
+/* Level-synchronous BFS on a device CSR graph (numpy_impl.py:114-131):
+ * levels[v] (-1 unreached); returns the eccentricity and visited count.
+ * Levels are independent of visit order, so equal to the reference. */
+mp_status mp_bfs_levels(int32_t n, const int64_t* indptr, const int32_t* indices, int32_t start, int32_t* levels,
+                        int32_t* ecc, int32_t* visited, void* stream);
+
+/* Block conflict DAG for the dataflow schedule: for every pair of blocks
+ * writing a common point, an edge from the lower to the higher
+ * (colour, id); order = blocks sorted by (key, id) where
+ * key(b) = max(b, max_pred key+1), a topological order close to id order. */
+mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offsets, const int32_t* written_ids,
+                            int64_t n_points, const int32_t* block_colours, int32_t num_colours,
+                            int32_t* pred_offsets /* [nb+1] */, int32_t* preds, int64_t preds_capacity,
+                            int64_t* num_preds, int32_t* order, void* stream);
+/* (when *num_preds > preds_capacity nothing but *num_preds is written:
+ *  grow the buffer and call again) */
+void mp_free(void* device_ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MESHPLAN_B200_H */

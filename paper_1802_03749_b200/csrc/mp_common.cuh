@@ -1,0 +1,65 @@
+// Shared helpers of the native library: status/error plumbing, dtype
+// dispatch, memory-order primitives.  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/meshplan_b200.h"
+
+namespace mp {
+
+// thread-local message of the last failing call (mp_last_error)
+void set_error(const char* fmt, ...);
+void clear_error();
+
+#define MP_CUDA_TRY(expr)                                                                 \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      ::mp::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__,       \
+                      __LINE__, cudaGetErrorString(_e));                                  \
+      return MP_ERR_CUDA;                                                                 \
+    }                                                                                     \
+  } while (0)
+
+#define MP_CHECK_LAUNCH() MP_CUDA_TRY(cudaGetLastError())
+
+#define MP_FAIL(code, ...)          \
+  do {                              \
+    ::mp::set_error(__VA_ARGS__);   \
+    return (code);                  \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- memory-order primitives -------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// L2-only load/store for data another CTA may have written this launch
+template <typename T>
+__device__ __forceinline__ T ld_cg(const T* p) { return __ldcg(p); }
+
+}  // namespace mp
+
+// dtype dispatch: calls F.template operator()<T>()
+#define MP_DISPATCH_DTYPE(dtype, ...)                           \
+  [&]() -> mp_status {                                          \
+    switch (dtype) {                                            \
+      case MP_F64: { using scalar_t = double; return __VA_ARGS__(); }  \
+      case MP_F32: { using scalar_t = float; return __VA_ARGS__(); }   \
+      case MP_I64: { using scalar_t = long long; return __VA_ARGS__(); } \
+      case MP_I32: { using scalar_t = int; return __VA_ARGS__(); }     \
+      default: MP_FAIL(MP_ERR_KERNEL, "unknown element type %d", (int)(dtype)); \
+    }                                                           \
+  }()

@@ -1,0 +1,365 @@
+// Graph-wide planner and checker kernels (CUB radix sorts + custom passes):
+//   * race check            (simulator.py:245-261, 446-469)
+//   * block conflict DAG + topological schedule for the dataflow executor
+//   * level-synchronous BFS (numpy_impl.py:114-131; levels are visit-order
+//     independent, so GPS levels equal the reference's)
+#include <cub/cub.cuh>
+#include <limits.h>
+
+#include "mp_common.cuh"
+
+namespace mp {
+namespace {
+
+// RAII scratch on the stream-ordered allocator
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t st;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes > 0 ? bytes : 1, st); }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  template <typename T> T* as() { return static_cast<T*>(p); }
+};
+
+template <typename K>
+cudaError_t sort_keys(K* keys, K* tmp_keys, int64_t n, cudaStream_t st, int end_bit = sizeof(K) * 8) {
+  cub::DoubleBuffer<K> db(keys, tmp_keys);
+  size_t bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, n, 0, end_bit, st);
+  if (e) return e;
+  Scratch tmp(st);
+  if ((e = tmp.alloc(bytes))) return e;
+  if ((e = cub::DeviceRadixSort::SortKeys(tmp.p, bytes, db, n, 0, end_bit, st))) return e;
+  if (db.Current() != keys) e = cudaMemcpyAsync(keys, db.Current(), n * sizeof(K), cudaMemcpyDeviceToDevice, st);
+  return e;
+}
+
+int bits_for(uint64_t maxval) {
+  int b = 1;
+  while (b < 64 && (maxval >> b)) ++b;
+  return b;
+}
+
+// ---- race check ----------------------------------------------------------------
+__global__ void race_keys_kernel(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ refs,
+                                 const int64_t* __restrict__ groups, int64_t span, uint64_t* keys, int32_t* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = groups[i];
+    for (int64_t j = off[i]; j < off[i + 1]; ++j) {
+      keys[j] = (uint64_t)(g * span + refs[j]);
+      vals[j] = (int32_t)i;
+    }
+  }
+}
+
+__global__ void first_dup_kernel(int64_t m, const uint64_t* __restrict__ keys, const int32_t* __restrict__ vals,
+                                 unsigned long long* first) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j + 1 < m; j += (int64_t)gridDim.x * blockDim.x)
+    if (keys[j] == keys[j + 1] && vals[j] != vals[j + 1]) atomicMin(first, (unsigned long long)j);
+}
+
+// ---- block DAG ------------------------------------------------------------------
+__global__ void point_block_keys(int32_t nb, const int32_t* __restrict__ off, const int32_t* __restrict__ ids,
+                                 uint64_t* keys) {
+  for (int b = blockIdx.x; b < nb; b += gridDim.x)
+    for (int j = off[b] + threadIdx.x; j < off[b + 1]; j += blockDim.x)
+      keys[j] = ((uint64_t)(uint32_t)ids[j] << 32) | (uint32_t)b;
+}
+
+// For each segment start (new point) count the block pairs of the segment.
+__global__ void seg_pair_count(int64_t m, const uint64_t* __restrict__ keys, int64_t* cnt) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    if (j == 0 || (keys[j] >> 32) != (keys[j - 1] >> 32)) {
+      int64_t e = j + 1;
+      while (e < m && (keys[e] >> 32) == (keys[j] >> 32)) ++e;
+      int64_t L = e - j;
+      c = L * (L - 1) / 2;
+    }
+    cnt[j] = c;
+  }
+}
+
+__global__ void seg_pair_emit(int64_t m, const uint64_t* __restrict__ keys, const int64_t* __restrict__ pos,
+                              const int32_t* __restrict__ colour, uint64_t* edges) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    if (!(j == 0 || (keys[j] >> 32) != (keys[j - 1] >> 32))) continue;
+    int64_t e = j + 1;
+    while (e < m && (keys[e] >> 32) == (keys[j] >> 32)) ++e;
+    int64_t w = pos[j];
+    for (int64_t a = j; a < e; ++a)
+      for (int64_t c = a + 1; c < e; ++c) {
+        uint32_t x = (uint32_t)keys[a], y = (uint32_t)keys[c];  // x < y (sorted by block)
+        // edge from the lower (colour, id) block to the higher one
+        bool x_first = colour[x] < colour[y] || (colour[x] == colour[y] && x < y);
+        uint32_t src = x_first ? x : y, dst = x_first ? y : x;
+        edges[w++] = ((uint64_t)dst << 32) | src;
+      }
+  }
+}
+
+__global__ void pred_offsets_kernel(int32_t nb, int64_t E, const uint64_t* __restrict__ edges, int32_t* off,
+                                    int32_t* preds) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nb; i += (int64_t)gridDim.x * blockDim.x) {
+    // first edge with dst >= i
+    int64_t lo = 0, hi = E;
+    const uint64_t key = (uint64_t)i << 32;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (edges[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    off[i] = (int32_t)lo;
+  }
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < E; j += (int64_t)gridDim.x * blockDim.x)
+    preds[j] = (int32_t)(uint32_t)edges[j];
+}
+
+__global__ void colour_keys_kernel(int32_t nb, const int32_t* __restrict__ colour, uint64_t* keys) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    keys[b] = ((uint64_t)(uint32_t)colour[b] << 32) | (uint32_t)b;
+}
+
+// key(b) = max(b, max over preds key(p) + 1) for the blocks of one colour
+__global__ void dag_key_kernel(int32_t lo, int32_t hi, const uint64_t* __restrict__ by_colour,
+                               const int32_t* __restrict__ off, const int32_t* __restrict__ preds, uint32_t* key) {
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = (uint32_t)by_colour[i];
+    uint32_t k = b;
+    for (int j = off[b]; j < off[b + 1]; ++j) {
+      uint32_t q = key[preds[j]] + 1;
+      k = q > k ? q : k;
+    }
+    key[b] = k;
+  }
+}
+
+__global__ void order_keys_kernel(int32_t nb, const uint32_t* __restrict__ key, uint64_t* keys) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    keys[b] = ((uint64_t)key[b] << 32) | (uint32_t)b;
+}
+
+__global__ void low_words_kernel(int64_t n, const uint64_t* __restrict__ keys, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)(uint32_t)keys[i];
+}
+
+// ---- BFS --------------------------------------------------------------------------
+__global__ void bfs_init(int32_t n, int32_t* levels, int32_t start, int32_t* frontier) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    levels[i] = (i == start) ? 0 : -1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) frontier[0] = start;
+}
+
+__global__ void bfs_expand(int32_t fsize, const int32_t* __restrict__ frontier, const int64_t* __restrict__ indptr,
+                           const int32_t* __restrict__ indices, int32_t* levels, int32_t next_level, int32_t* next,
+                           int32_t* next_size) {
+  // one warp per frontier node, lanes over its neighbours
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < fsize;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t u = frontier[w];
+    for (int64_t j = indptr[u] + lane; j < indptr[u + 1]; j += 32) {
+      const int32_t v = indices[j];
+      if (levels[v] < 0 && atomicCAS(&levels[v], -1, next_level) == -1) next[atomicAdd(next_size, 1)] = v;
+    }
+  }
+}
+
+inline int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
+}  // namespace
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" mp_status mp_race_check(int64_t n, const int64_t* ref_offsets, const int32_t* refs, const int64_t* groups,
+                                   int64_t key_span, int64_t* first_pair, void* stream) {
+  clear_error();
+  first_pair[0] = first_pair[1] = -1;
+  if (n == 0) return MP_OK;
+  cudaStream_t st = as_stream(stream);
+  int64_t m = 0;
+  MP_CUDA_TRY(cudaMemcpyAsync(&m, ref_offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  MP_CUDA_TRY(cudaStreamSynchronize(st));
+  if (m < 2) return MP_OK;
+  Scratch keys(st), keys2(st), vals(st), vals2(st), tmp(st), first(st);
+  MP_CUDA_TRY(keys.alloc(m * 8));
+  MP_CUDA_TRY(keys2.alloc(m * 8));
+  MP_CUDA_TRY(vals.alloc(m * 4));
+  MP_CUDA_TRY(vals2.alloc(m * 4));
+  MP_CUDA_TRY(first.alloc(8));
+  race_keys_kernel<<<grid_for(n), 256, 0, st>>>(n, ref_offsets, refs, groups, key_span, keys.as<uint64_t>(),
+                                                 vals.as<int32_t>());
+  MP_CHECK_LAUNCH();
+  cub::DoubleBuffer<uint64_t> dk(keys.as<uint64_t>(), keys2.as<uint64_t>());
+  cub::DoubleBuffer<int32_t> dv(vals.as<int32_t>(), vals2.as<int32_t>());
+  size_t bytes = 0;
+  MP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, dk, dv, m, 0, 64, st));
+  MP_CUDA_TRY(tmp.alloc(bytes));
+  MP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, dk, dv, m, 0, 64, st));
+  unsigned long long none = ~0ull;
+  MP_CUDA_TRY(cudaMemcpyAsync(first.p, &none, 8, cudaMemcpyHostToDevice, st));
+  first_dup_kernel<<<grid_for(m), 256, 0, st>>>(m, dk.Current(), dv.Current(), first.as<unsigned long long>());
+  MP_CHECK_LAUNCH();
+  unsigned long long j = none;
+  MP_CUDA_TRY(cudaMemcpyAsync(&j, first.p, 8, cudaMemcpyDeviceToHost, st));
+  MP_CUDA_TRY(cudaStreamSynchronize(st));
+  if (j != none) {
+    int32_t pair[2];
+    MP_CUDA_TRY(cudaMemcpyAsync(pair, dv.Current() + j, 8, cudaMemcpyDeviceToHost, st));
+    MP_CUDA_TRY(cudaStreamSynchronize(st));
+    first_pair[0] = pair[0];
+    first_pair[1] = pair[1];
+  }
+  return MP_OK;
+}
+
+extern "C" mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offsets, const int32_t* written_ids,
+                                       int64_t n_points, const int32_t* block_colours, int32_t num_colours,
+                                       int32_t* pred_offsets, int32_t* preds, int64_t preds_capacity,
+                                       int64_t* num_preds, int32_t* order, void* stream) {
+  clear_error();
+  *num_preds = 0;
+  if (nb == 0) return MP_OK;
+  cudaStream_t st = as_stream(stream);
+  int32_t m32 = 0;
+  MP_CUDA_TRY(cudaMemcpyAsync(&m32, written_offsets + nb, 4, cudaMemcpyDeviceToHost, st));
+  MP_CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t m = m32;
+  Scratch keys(st), keys2(st), cnt(st), pos(st), tmp(st);
+  MP_CUDA_TRY(keys.alloc(m * 8));
+  MP_CUDA_TRY(keys2.alloc(m * 8));
+  point_block_keys<<<grid_for(nb, 1), 128, 0, st>>>(nb, written_offsets, written_ids, keys.as<uint64_t>());
+  MP_CHECK_LAUNCH();
+  MP_CUDA_TRY(sort_keys(keys.as<uint64_t>(), keys2.as<uint64_t>(), m, st));
+  MP_CUDA_TRY(cnt.alloc((m + 1) * 8));
+  MP_CUDA_TRY(pos.alloc((m + 1) * 8));
+  seg_pair_count<<<grid_for(m), 256, 0, st>>>(m, keys.as<uint64_t>(), cnt.as<int64_t>());
+  MP_CHECK_LAUNCH();
+  MP_CUDA_TRY(cudaMemsetAsync(cnt.as<int64_t>() + m, 0, 8, st));
+  size_t bytes = 0;
+  MP_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.as<int64_t>(), pos.as<int64_t>(), m + 1, st));
+  MP_CUDA_TRY(tmp.alloc(bytes));
+  MP_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.as<int64_t>(), pos.as<int64_t>(), m + 1, st));
+  int64_t E = 0;
+  MP_CUDA_TRY(cudaMemcpyAsync(&E, pos.as<int64_t>() + m, 8, cudaMemcpyDeviceToHost, st));
+  MP_CUDA_TRY(cudaStreamSynchronize(st));
+
+  Scratch edges(st), edges2(st), uniq(st), nuniq(st), tmp2(st);
+  MP_CUDA_TRY(edges.alloc(E * 8));
+  MP_CUDA_TRY(edges2.alloc(E * 8));
+  if (E > 0) {
+    seg_pair_emit<<<grid_for(m), 256, 0, st>>>(m, keys.as<uint64_t>(), pos.as<int64_t>(), block_colours,
+                                                edges.as<uint64_t>());
+    MP_CHECK_LAUNCH();
+    MP_CUDA_TRY(sort_keys(edges.as<uint64_t>(), edges2.as<uint64_t>(), E, st));
+  }
+  MP_CUDA_TRY(uniq.alloc(E * 8));
+  MP_CUDA_TRY(nuniq.alloc(8));
+  int64_t U = 0;
+  if (E > 0) {
+    bytes = 0;
+    MP_CUDA_TRY(cub::DeviceSelect::Unique(nullptr, bytes, edges.as<uint64_t>(), uniq.as<uint64_t>(),
+                                          nuniq.as<int64_t>(), E, st));
+    MP_CUDA_TRY(tmp2.alloc(bytes));
+    MP_CUDA_TRY(cub::DeviceSelect::Unique(tmp2.p, bytes, edges.as<uint64_t>(), uniq.as<uint64_t>(),
+                                          nuniq.as<int64_t>(), E, st));
+    MP_CUDA_TRY(cudaMemcpyAsync(&U, nuniq.p, 8, cudaMemcpyDeviceToHost, st));
+    MP_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  *num_preds = U;
+  if (U > preds_capacity) return MP_OK;  // caller grows the buffer and calls again
+  pred_offsets_kernel<<<grid_for(nb + 1 > U ? nb + 1 : U), 256, 0, st>>>(nb, U, uniq.as<uint64_t>(), pred_offsets,
+                                                                          preds);
+  MP_CHECK_LAUNCH();
+
+  // blocks grouped by colour, then keys colour by colour
+  Scratch ck(st), ck2(st), key(st);
+  MP_CUDA_TRY(ck.alloc(nb * 8));
+  MP_CUDA_TRY(ck2.alloc(nb * 8));
+  MP_CUDA_TRY(key.alloc(nb * 4));
+  colour_keys_kernel<<<grid_for(nb), 256, 0, st>>>(nb, block_colours, ck.as<uint64_t>());
+  MP_CHECK_LAUNCH();
+  MP_CUDA_TRY(sort_keys(ck.as<uint64_t>(), ck2.as<uint64_t>(), nb, st));
+  // host copy of colour boundaries
+  uint64_t* hk = (uint64_t*)malloc(nb * 8);
+  if (!hk) MP_FAIL(MP_ERR_CUDA, "host allocation failed");
+  cudaError_t ce = cudaMemcpyAsync(hk, ck.p, nb * 8, cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) {
+    free(hk);
+    MP_CUDA_TRY(ce);
+  }
+  int32_t lo = 0;
+  while (lo < nb) {
+    uint32_t c = (uint32_t)(hk[lo] >> 32);
+    int32_t hi = lo;
+    while (hi < nb && (uint32_t)(hk[hi] >> 32) == c) ++hi;
+    dag_key_kernel<<<grid_for(hi - lo), 256, 0, st>>>(lo, hi, ck.as<uint64_t>(), pred_offsets, preds,
+                                                     key.as<uint32_t>());
+    ce = cudaGetLastError();
+    if (ce != cudaSuccess) break;
+    lo = hi;
+  }
+  free(hk);
+  MP_CUDA_TRY(ce);
+  order_keys_kernel<<<grid_for(nb), 256, 0, st>>>(nb, key.as<uint32_t>(), ck.as<uint64_t>());
+  MP_CHECK_LAUNCH();
+  MP_CUDA_TRY(sort_keys(ck.as<uint64_t>(), ck2.as<uint64_t>(), nb, st));
+  low_words_kernel<<<grid_for(nb), 256, 0, st>>>(nb, ck.as<uint64_t>(), order);
+  MP_CHECK_LAUNCH();
+  MP_CUDA_TRY(cudaStreamSynchronize(st));
+  (void)n_points;
+  (void)num_colours;
+  return MP_OK;
+}
+
+extern "C" mp_status mp_bfs_levels(int32_t n, const int64_t* indptr, const int32_t* indices, int32_t start,
+                                   int32_t* levels, int32_t* ecc, int32_t* visited, void* stream) {
+  clear_error();
+  *ecc = 0;
+  *visited = 0;
+  if (n == 0) return MP_OK;
+  if (start < 0 || start >= n) MP_FAIL(MP_ERR_VALIDATION, "bfs start %d out of range", start);
+  cudaStream_t st = as_stream(stream);
+  Scratch fa(st), fb(st), cnt(st);
+  MP_CUDA_TRY(fa.alloc((size_t)n * 4));
+  MP_CUDA_TRY(fb.alloc((size_t)n * 4));
+  MP_CUDA_TRY(cnt.alloc(4));
+  int32_t* pinned = nullptr;
+  MP_CUDA_TRY(cudaMallocHost(&pinned, 4));
+  bfs_init<<<grid_for(n), 256, 0, st>>>(n, levels, start, fa.as<int32_t>());
+  cudaError_t ce = cudaGetLastError();
+  int32_t fsize = 1, total = 1, level = 0;
+  int32_t *cur = fa.as<int32_t>(), *nxt = fb.as<int32_t>();
+  while (ce == cudaSuccess && fsize > 0) {
+    ce = cudaMemsetAsync(cnt.p, 0, 4, st);
+    if (ce) break;
+    int64_t threads = (int64_t)fsize * 32;
+    int grid = (int)((threads + 255) / 256 < 148 * 16 ? (threads + 255) / 256 : 148 * 16);
+    bfs_expand<<<grid, 256, 0, st>>>(fsize, cur, indptr, indices, levels, level + 1, nxt, cnt.as<int32_t>());
+    if ((ce = cudaGetLastError())) break;
+    if ((ce = cudaMemcpyAsync(pinned, cnt.p, 4, cudaMemcpyDeviceToHost, st))) break;
+    if ((ce = cudaStreamSynchronize(st))) break;
+    fsize = *pinned;
+    if (fsize > 0) {
+      ++level;
+      total += fsize;
+      int32_t* t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+  }
+  cudaFreeHost(pinned);
+  MP_CUDA_TRY(ce);
+  *ecc = level;
+  *visited = total;
+  return MP_OK;
+}

@@ -1,0 +1,464 @@
+"""Executors: run a loop under a plan on the GPU (Seam B of the reference).
+
+``execute_global`` / ``execute_hierarchical`` / ``execute_serial`` keep the
+reference signatures and return values (simulator.py:215, 355, 525): they
+take the plan's host mesh, copy the loop's arrays to the device, launch the
+sm_100a executors through the C ABI, copy the incremented array back and
+return ``(result_mesh, MetricsReport)`` in plan numbering.  Like the
+reference they *check* plans instead of trusting them -- colour races at both
+levels, block widths, shared capacity and staging coverage are verified on
+the GPU before any output is produced (once per plan object and kernel).
+
+``DeviceLoop`` is the resident form for time-stepping codes and the
+benchmark: arrays stay in HBM and ``run()`` only launches.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native, gpuplan
+from .errors import CapacityError, KernelSpecError, RaceError
+from .kernelspec import KernelSpec
+from .mesh import DataArray, Mesh
+from .plan import GlobalPlan, HierarchicalPlan, MAPPING_ENTRY_BYTES, reuse_factor
+
+SCHEDULES = {"colour": _native.MP_SCHED_COLOUR, "dataflow": _native.MP_SCHED_DATAFLOW}
+TORCH_DTYPES = {"f64": torch.float64, "f32": torch.float32, "i64": torch.int64, "i32": torch.int32}
+
+
+# ------------------------------------------------------------------------------
+# metrics
+# ------------------------------------------------------------------------------
+
+
+@dataclass
+class MetricsReport:
+    """Plan-derived and measured metrics of one loop execution.
+
+    Field names follow the reference report (simulator.py:264-312).  The
+    reference's cache-line transaction counts and bandwidth proxy are a cost
+    model of a P100; here those fields stay ``None`` and the measured
+    ``device_ms`` / ``effective_gbps`` (useful bytes / device time, the
+    paper's formula) replace them.
+    """
+
+    strategy: str
+    n_elements: int
+    num_launches: int
+    block_colours: int
+    useful_bytes: int
+    temp_array_bytes: int
+    atomic_ops: int
+    occupancy_estimate: float = 0.0
+    blocks_per_sm: int = 0
+    reuse_factor: float | None = None
+    thread_colours_max: int | None = None
+    thread_colours_mean: float | None = None
+    sync_count: int = 0
+    sync_counts: np.ndarray | None = None
+    shared_bytes_max: int = 0
+    num_blocks: int = 0
+    schedule: str | None = None
+    device_ms: float | None = None
+    effective_gbps: float | None = None
+    read_transactions: int | None = None
+    write_transactions: int | None = None
+    bandwidth_proxy: float | None = None
+
+    def to_dict(self) -> dict:
+        out = {}
+        for k, v in self.__dict__.items():
+            if isinstance(v, np.ndarray):
+                v = v.tolist()
+            elif isinstance(v, np.integer):
+                v = int(v)
+            elif isinstance(v, np.floating):
+                v = float(v)
+            out[k] = v
+        return out
+
+
+def useful_bytes(kernel: KernelSpec, mesh: Mesh) -> int:
+    """Paper bandwidth numerator (simulator.py:315-328): every array once,
+    incremented arrays twice, plus 4-byte mapping entries."""
+    total, seen = 0, set()
+    for a in kernel.args:
+        if a.array in seen:
+            continue
+        seen.add(a.array)
+        arr = mesh.data[a.array]
+        total += (2 if a.mode == "increment" else 1) * arr.set.size * arr.components * arr.values.dtype.itemsize
+    for name in kernel.mapping_names():
+        m = mesh.mappings[name]
+        total += m.from_set.size * m.arity * MAPPING_ENTRY_BYTES
+    return total
+
+
+def _alt_costs(kernel, mesh):
+    n = mesh.sets[kernel.iter_set_name(mesh)].size
+    tb = ops = 0
+    for a in kernel.increment_args:
+        arr = mesh.data[a.array]
+        k = len(kernel.arg_slots(mesh, a))
+        tb += n * k * arr.components * arr.values.dtype.itemsize
+        ops += n * k * arr.components
+    return tb, ops
+
+
+def estimate_occupancy(threads: int, shared_bytes: int, regs: int, hw):
+    """Resident blocks/SM and occupancy (simulator.py:63-103)."""
+    warps = -(-threads // hw.warp_size)
+    rpw = -(-regs * hw.warp_size // hw.reg_alloc_granularity) * hw.reg_alloc_granularity
+    rpb = warps * rpw
+    if (threads > hw.max_threads_per_block or regs > hw.max_registers_per_thread
+            or shared_bytes > hw.shared_bytes_per_sm or rpb > hw.registers_per_sm):
+        return 0, 0.0
+    blocks = min(hw.max_blocks_per_sm, hw.max_threads_per_sm // threads, hw.max_warps_per_sm // warps,
+                 hw.registers_per_sm // rpb)
+    if shared_bytes > 0:
+        blocks = min(blocks, hw.shared_bytes_per_sm // shared_bytes)
+    return int(blocks), blocks * warps * hw.warp_size / hw.max_threads_per_sm
+
+
+# ------------------------------------------------------------------------------
+# binding a kernel to device arrays
+# ------------------------------------------------------------------------------
+
+
+def _roles(kernel: KernelSpec):
+    if kernel.device_op is None:
+        raise KernelSpecError(
+            f"kernel {kernel.name!r} has no device functor; registered ops are {sorted(_native.OPS)} "
+            "(there is no CPU fallback)"
+        )
+    op, _, variant = kernel.device_op.partition(":")
+    if op not in _native.OPS:
+        raise KernelSpecError(f"unknown device op {kernel.device_op!r}")
+    ind = [a for a in kernel.args if a.indirect and a.mode == "read"]
+    dirs = [a for a in kernel.args if not a.indirect and a.mode == "read"]
+    incs = [a for a in kernel.args if a.mode == "increment"]
+    if len(ind) > 1 or len(dirs) != 1 or len(incs) != 1 or any(a.mode == "write" for a in kernel.args):
+        raise KernelSpecError(f"kernel {kernel.name!r}: argument shape does not match device op {op!r}")
+    return _native.OPS[op], variant == "unit", (ind[0] if ind else None), dirs[0], incs[0]
+
+
+@dataclass
+class DeviceLoop:
+    """A kernel bound to a plan with its arrays resident in HBM (plan numbering)."""
+
+    plan: object
+    kernel: KernelSpec
+    tensors: dict
+    loop: _native.MpLoop
+    schedule: int = _native.MP_SCHED_DATAFLOW
+    launches: int = 0
+    _keep: list = field(default_factory=list)
+
+    def run(self, stream=None) -> None:
+        """Launch one full execution of the loop (all colours); asynchronous."""
+        sp = _native.stream_ptr(stream)
+        dp = self.plan._device
+        if isinstance(self.plan, GlobalPlan):
+            offs = np.ascontiguousarray(dp.colour_offsets, dtype=np.int64)
+            _native.call("mp_exec_global", self.loop, offs.ctypes.data, len(offs) - 1,
+                         int(self.plan.config.block_size), sp)
+        else:
+            dp.epoch += 1
+            _native.call("mp_exec_hier", self.loop, dp.struct_cached(), self.schedule, dp.epoch & 0xFFFFFFFF, sp)
+
+    def run_host(self, inputs: dict, out, stream=None) -> None:
+        """One end-to-end step with host buffers: H2D of the given arrays
+        (name -> pinned numpy / torch, plan numbering), the launch, and D2H of
+        the incremented array into ``out``; all on one stream, asynchronous."""
+        import warnings
+
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)  # read-only numpy views of pinned buffers
+            for name, host in inputs.items():
+                src = torch.from_numpy(host) if isinstance(host, np.ndarray) else host
+                self.tensors[name].copy_(src.reshape(self.tensors[name].shape), non_blocking=True)
+        self.run(stream)
+        inc = next(a.array for a in self.kernel.args if a.mode == "increment")
+        dst = torch.from_numpy(out) if isinstance(out, np.ndarray) else out
+        dst.copy_(self.tensors[inc].reshape(dst.shape), non_blocking=True)
+
+    def launches_per_run(self) -> int:
+        if isinstance(self.plan, GlobalPlan):
+            return int(np.count_nonzero(np.diff(self.plan._device.colour_offsets)))
+        if self.schedule == _native.MP_SCHED_DATAFLOW:
+            return 1 if self.plan.num_blocks else 0
+        return int(np.count_nonzero(np.diff(self.plan._device.colour_block_offsets)))
+
+
+def _array_tensor(arr: DataArray, dev) -> torch.Tensor:
+    host = torch.from_numpy(np.ascontiguousarray(arr.values))
+    return host.to(dev, non_blocking=True)
+
+
+def bind(plan, kernel: KernelSpec, tensors: dict | None = None, schedule: str = "dataflow") -> DeviceLoop:
+    """Bind ``kernel`` to ``plan``; ``tensors`` (name -> device tensor in plan
+    numbering and plan layout) default to uploads of ``plan.mesh``."""
+    if kernel.signature_key() != plan.kernel_key:
+        raise KernelSpecError("plan was built for a different kernel signature")
+    mesh = plan.mesh
+    kernel.validate_against(mesh)
+    op, unit, ind, dr, inc = _roles(kernel)
+    ensure_device(plan, kernel)
+    dev = torch.device("cuda")
+    t = dict(tensors or {})
+    for a in (ind, dr, inc):
+        if a is not None and a.array not in t:
+            t[a.array] = _array_tensor(mesh.data[a.array], dev)
+    inc_arr = mesh.data[inc.array]
+    dtypes = {mesh.data[a.array].elem_type for a in (ind, dr, inc) if a is not None}
+    if len(dtypes) != 1:
+        raise KernelSpecError(f"kernel {kernel.name!r}: device ops need one element type, got {sorted(dtypes)}")
+    m = mesh.mappings[inc.mapping]
+    L = _native.MpLoop()
+    L.op, L.unit, L.dtype = op, int(unit), _native.DTYPES[inc_arr.elem_type]
+    L.ind_layout = _native.LAYOUTS[inc_arr.layout]
+    if ind is not None and mesh.data[ind.array].layout != inc_arr.layout:
+        raise KernelSpecError("indirect arrays of one loop must share a layout")
+    L.n_elems, L.n_points, L.arity = m.from_set.size, m.to_set.size, m.arity
+    L.map_layout = _native.MP_AOS
+    L.map = plan._device.map.data_ptr()
+    if ind is not None:
+        L.ind_read = t[ind.array].data_ptr()
+        L.ind_read_comps = mesh.data[ind.array].components
+    L.dir_read = t[dr.array].data_ptr()
+    L.dir_comps = mesh.data[dr.array].components
+    L.inc = t[inc.array].data_ptr()
+    L.inc_comps = inc_arr.components
+    return DeviceLoop(plan, kernel, t, L, SCHEDULES[schedule])
+
+
+# ------------------------------------------------------------------------------
+# device state + verification (once per plan object and kernel)
+# ------------------------------------------------------------------------------
+
+
+def _struct_cached(self):
+    s = getattr(self, "_struct", None)
+    if s is None:
+        s = self.struct()
+        self._struct = s
+    return s
+
+
+gpuplan.DevicePlan.struct_cached = _struct_cached
+
+
+def ensure_device(plan, kernel: KernelSpec) -> None:
+    verified = getattr(plan, "_verified", None)
+    if verified is not None and kernel.signature_key() in verified:
+        return
+    _native.require_cuda()
+    if getattr(plan, "_device", None) is None:
+        object.__setattr__(plan, "_device", _device_from_host(plan, kernel))
+    if isinstance(plan, GlobalPlan):
+        _verify_global(plan, kernel)
+    else:
+        _verify_hier(plan, kernel)
+    object.__setattr__(plan, "_verified", (verified or set()) | {kernel.signature_key()})
+
+
+def _kernel_map(plan, kernel) -> torch.Tensor:
+    m = gpuplan.single_mapping(plan.mesh, kernel)
+    if m is None:
+        raise KernelSpecError(f"kernel {kernel.name!r} has no indirect argument")
+    return torch.as_tensor(m.table, device="cuda").to(torch.int32).contiguous()
+
+
+def _device_from_host(plan, kernel):
+    """Device structures for a plan that was loaded or edited on the host."""
+    from .builder import GlobalDevicePlan
+
+    map_d = _kernel_map(plan, kernel)
+    if isinstance(plan, GlobalPlan):
+        return GlobalDevicePlan(map_d, np.asarray(plan.colour_offsets, dtype=np.int64))
+    mesh = plan.mesh
+    m = gpuplan.single_mapping(mesh, kernel)
+    dev = map_d.device
+    offsets = np.asarray(plan.block_offsets, dtype=np.int64)
+    gpuplan.check_block_widths(offsets, plan.config.block_size)
+    name = m.to_set.name
+    i32 = lambda a: torch.as_tensor(np.asarray(a, dtype=np.int32), device=dev)  # noqa: E731
+    empty = (np.zeros(len(offsets), dtype=np.int64), np.zeros(0, dtype=np.int64))
+    st = plan.staged.get(name, empty)
+    wr = plan.written.get(name, empty)
+    staged_args = kernel.indirect_args if plan.config.staging == "all-indirect" else kernel.increment_args
+    smask = gpuplan.slot_mask(kernel, mesh, staged_args)
+    try:
+        return gpuplan.build_device_hier(
+            map_d, offsets, np.asarray(plan.block_colours.colours, dtype=np.int64), plan.block_colours.num_colours,
+            i32(plan.thread_colours), i32(plan.thread_colour_counts), i32(st[0]), i32(st[1]), i32(wr[0]), i32(wr[1]),
+            smask, plan.config.staging == "all-indirect", m.to_set.size,
+            int(np.diff(offsets).max()) if offsets.size > 1 else 0,
+        )
+    except CapacityError as exc:
+        raise CapacityError(f"{exc} on set {name!r}") from None
+
+
+def _race(n_items, ref_off, refs, groups, span, what, fmt):
+    pair = np.full(2, -1, dtype=np.int64)
+    _native.call("mp_race_check", int(n_items), _native.ptr(ref_off), _native.ptr(refs), _native.ptr(groups),
+                 int(span), pair.ctypes.data, _native.stream_ptr())
+    if pair[0] >= 0:
+        raise RaceError(fmt(int(pair[0]), int(pair[1])))
+
+
+def _element_refs(plan, kernel, map_d):
+    wslots = sorted({s for a in kernel.increment_args for s in kernel.arg_slots(plan.mesh, a)})
+    n = map_d.shape[0]
+    refs = map_d[:, wslots].contiguous().reshape(-1)
+    off = torch.arange(n + 1, dtype=torch.long, device=map_d.device) * len(wslots)
+    return off, refs
+
+
+def _verify_global(plan: GlobalPlan, kernel) -> None:
+    dp = plan._device
+    n = dp.map.shape[0]
+    offs = np.asarray(plan.colour_offsets, dtype=np.int64)
+    colour_of = np.repeat(np.arange(len(offs) - 1, dtype=np.int64), np.diff(offs))
+    if colour_of.size != n:
+        raise RaceError("global colouring: colour ranges do not cover the iteration set")
+    g = torch.as_tensor(colour_of, device="cuda")
+    off, refs = _element_refs(plan, kernel, dp.map)
+    span = int(plan.mesh.mappings[kernel.increment_args[0].mapping].to_set.size) + 1
+    _race(n, off, refs, g, span, "global",
+          lambda a, b: f"global colouring: elements {a} and {b} share group {int(colour_of[a])} but write a common point")
+
+
+def _verify_hier(plan: HierarchicalPlan, kernel) -> None:
+    dp = plan._device
+    offsets = np.asarray(plan.block_offsets, dtype=np.int64)
+    n = dp.map.shape[0]
+    nb = offsets.size - 1
+    if nb and int(np.diff(offsets).max()) > plan.config.block_size:
+        raise CapacityError("plan contains a block wider than the configured block size")
+    block_of = np.repeat(np.arange(nb, dtype=np.int64), np.diff(offsets))
+    tmax = int(np.asarray(plan.thread_colour_counts).max(initial=0))
+    groups = block_of * np.int64(max(tmax, 1) + 1) + np.asarray(plan.thread_colours, dtype=np.int64)
+    off, refs = _element_refs(plan, kernel, dp.map)
+    m = plan.mesh.mappings[kernel.increment_args[0].mapping]
+    span = m.to_set.size + 1
+    _race(n, off, refs, torch.as_tensor(groups, device="cuda"), span, "thread",
+          lambda a, b: f"thread colouring: elements {a} and {b} share group {int(groups[a])} but write a common point")
+    bcol = np.asarray(plan.block_colours.colours, dtype=np.int64)
+    for set_name, (indptr, ids) in plan.written.items():
+        _race(nb, torch.as_tensor(np.asarray(indptr, dtype=np.int64), device="cuda"),
+              torch.as_tensor(np.asarray(ids, dtype=np.int32), device="cuda"), torch.as_tensor(bcol, device="cuda"),
+              span, "block",
+              lambda a, b, s=set_name: f"block colouring: blocks {a} and {b} share a colour but write a common "
+                                       f"point of set {s!r}")
+    limit = plan.hw.shared_bytes_per_sm
+    if nb and int(plan.shared_bytes.max()) > limit:
+        b = int(plan.shared_bytes.argmax())
+        raise CapacityError(f"block {b} needs {int(plan.shared_bytes[b])} shared bytes, over the {limit}-byte limit")
+
+
+# ------------------------------------------------------------------------------
+# reference-compatible entry points
+# ------------------------------------------------------------------------------
+
+
+def _report(plan, kernel, loop: DeviceLoop, ms: float | None) -> MetricsReport:
+    mesh = plan.mesh
+    ub = useful_bytes(kernel, mesh)
+    tb, ops = _alt_costs(kernel, mesh)
+    n = mesh.sets[kernel.iter_set_name(mesh)].size
+    gbps = (ub / (ms * 1e-3) / 1e9) if ms else None
+    if isinstance(plan, GlobalPlan):
+        bps, occ = estimate_occupancy(plan.config.block_size, 0, kernel.regs_per_thread, plan.hw)
+        return MetricsReport("global", n, plan.num_colours, plan.num_colours, ub, tb, ops, occ, bps,
+                             num_blocks=int(sum(-(-int(c) // plan.config.block_size) for c in np.diff(plan.colour_offsets))),
+                             device_ms=ms, effective_gbps=gbps)
+    nb = plan.num_blocks
+    sync = plan.thread_colour_counts + 2
+    smax = int(plan.shared_bytes.max()) if nb else 0
+    bps, occ = estimate_occupancy(plan.config.block_size, smax, kernel.regs_per_thread, plan.hw)
+    return MetricsReport(
+        "hier", n, loop.launches_per_run(), plan.block_colours.num_colours, ub, tb, ops, occ, bps,
+        reuse_factor(plan), int(plan.thread_colour_counts.max()) if nb else 0,
+        float(plan.thread_colour_counts.mean()) if nb else 0.0, int(sync.sum()) if nb else 0, sync, smax, nb,
+        "dataflow" if loop.schedule == _native.MP_SCHED_DATAFLOW else "colour", ms, gbps,
+    )
+
+
+def _run_and_collect(plan, kernel, schedule="dataflow"):
+    loop = bind(plan, kernel, schedule=schedule)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    loop.run()
+    stop.record()
+    inc = next(a for a in kernel.args if a.mode == "increment")
+    out = loop.tensors[inc.array].cpu().numpy()
+    ms = start.elapsed_time(stop)
+    arr = plan.mesh.data[inc.array]
+    result = plan.mesh.with_data(DataArray(arr.name, arr.set, arr.components, out, arr.layout))
+    return result, _report(plan, kernel, loop, ms)
+
+
+def execute_global(plan: GlobalPlan, kernel: KernelSpec):
+    """One launch per colour range; returns (plan-numbered result, report)."""
+    if not isinstance(plan, GlobalPlan):
+        raise KernelSpecError("execute_global needs a GlobalPlan")
+    return _run_and_collect(plan, kernel)
+
+
+def execute_hierarchical(plan: HierarchicalPlan, kernel: KernelSpec, schedule: str = "dataflow"):
+    """Hierarchical shared-memory execution; ``schedule`` is ``"dataflow"``
+    (one launch, DAG-ordered blocks) or ``"colour"`` (one launch per block
+    colour, the paper's scheme).  Both give bit-identical results."""
+    if not isinstance(plan, HierarchicalPlan):
+        raise KernelSpecError("execute_hierarchical needs a HierarchicalPlan")
+    return _run_and_collect(plan, kernel, schedule)
+
+
+def execute_serial(mesh: Mesh, kernel: KernelSpec) -> Mesh:
+    """Element-order semantics of the reference oracle, computed on the GPU:
+    temp-array increments + per-point ordered folds (bit-identical to
+    np.add.at order for every input)."""
+    kernel.validate_against(mesh)
+    op, unit, ind, dr, inc = _roles(kernel)
+    m = gpuplan.single_mapping(mesh, kernel)
+    _native.require_cuda()
+    dev = torch.device("cuda")
+    n, ar = m.from_set.size, m.arity
+    map_d = torch.as_tensor(m.table, device=dev).to(torch.int32).reshape(n, ar)
+    wslots = sorted(kernel.arg_slots(mesh, inc))
+    flat = map_d.long().reshape(-1)
+    pos = torch.arange(n * ar, dtype=torch.long, device=dev)
+    in_w = (pos % max(ar, 1)).unsqueeze(0) == torch.as_tensor(wslots, device=dev).unsqueeze(1) if wslots else None
+    sel = in_w.any(0) if in_w is not None else torch.zeros_like(pos, dtype=torch.bool)
+    keys, order = torch.sort(flat[sel], stable=True)
+    refs = pos[sel][order]
+    # temp is indexed by e*arity + s of the op's own slot loop
+    off = torch.zeros(m.to_set.size + 1, dtype=torch.int32, device=dev)
+    if keys.numel():
+        off[1:] = torch.cumsum(torch.bincount(keys, minlength=m.to_set.size), 0).to(torch.int32)
+    arrays = {}
+    for a in (ind, dr, inc):
+        if a is not None:
+            x = mesh.data[a.array]
+            lay = x.layout if a.indirect else "soa"
+            v2 = np.ascontiguousarray(x.view2d())
+            flat_v = v2.T.ravel() if lay == "soa" else v2.ravel()
+            arrays[a.array] = (torch.as_tensor(np.ascontiguousarray(flat_v), device=dev), lay)
+    inc_arr = mesh.data[inc.array]
+    L = _native.MpLoop()
+    L.op, L.unit, L.dtype = op, int(unit), _native.DTYPES[inc_arr.elem_type]
+    L.ind_layout = _native.LAYOUTS[arrays[inc.array][1]]
+    L.n_elems, L.n_points, L.arity, L.map_layout = n, m.to_set.size, ar, _native.MP_AOS
+    L.map = map_d.data_ptr()
+    if ind is not None:
+        L.ind_read, L.ind_read_comps = arrays[ind.array][0].data_ptr(), mesh.data[ind.array].components
+    L.dir_read, L.dir_comps = arrays[dr.array][0].data_ptr(), mesh.data[dr.array].components
+    L.inc, L.inc_comps = arrays[inc.array][0].data_ptr(), inc_arr.components
+    temp = torch.empty(max(n * ar * inc_arr.components, 1), dtype=TORCH_DTYPES[inc_arr.elem_type], device=dev)
+    refs32 = refs.to(torch.int32)
+    _native.call("mp_exec_serial", L, off.data_ptr(), refs32.data_ptr(), temp.data_ptr(), _native.stream_ptr())
+    out = arrays[inc.array][0].cpu().numpy()
+    return mesh.with_data(DataArray(inc_arr.name, inc_arr.set, inc_arr.components, out, arrays[inc.array][1]))

@@ -1,0 +1,353 @@
+"""Device plan builder: the reference planner's steps, run on the GPU.
+
+Each step cites the reference function whose result it reproduces
+bit for bit (pkg/src/meshplan/plan.py, reorder.py, colouring.py):
+
+=======================  ==========================================  ==================
+step                      reference                                   where it runs
+=======================  ==========================================  ==================
+point graph               reorder.mesh_to_graph (63-79)               GPU (sort/unique)
+GPS levels + root         reorder.gps_renumber (95-141)               GPU BFS (native)
+element lex sort          reorder.lex_sort_elements (161-171)         GPU stable sorts
+chunk / structured        partition.chunk_partition, structured       host arithmetic
+split oversized           plan._split_oversized (451-464)             host (nb-sized)
+per-block written lists   plan._colour_blocks_ns (241-257)            GPU, CTA per block
+block colouring           greedy_colour_csr least-loaded              native host C++
+thread colouring + sort   plan._thread_colours_for_block (260-284)    GPU, warp per block
+staged / written CSR      plan._per_block_point_lists (582-603)       GPU, CTA per block
+shared slots              HierarchicalPlan.staged_slots (168-182)     GPU (materialised)
+element colouring         plan._colour_elements (232-238)             native host C++
+dataflow DAG + order      (new: the dataflow schedule)                GPU
+=======================  ==========================================  ==================
+
+Device tensors that the executors need stay resident in a ``DevicePlan``.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import CapacityError, KernelSpecError, MeshValidationError
+from .mesh import DataArray, Mapping, Mesh
+
+DEV = "cuda"
+
+
+def _dev() -> torch.device:
+    _native.require_cuda()
+    return torch.device(DEV)
+
+
+def _sp():
+    return _native.stream_ptr()
+
+
+def single_mapping(mesh: Mesh, kernel) -> Mapping | None:
+    """The one mapping a device-executable loop may use (None: no indirection)."""
+    names = kernel.mapping_names()
+    if not names:
+        return None
+    if len(names) > 1:
+        raise KernelSpecError(
+            f"kernel {kernel.name!r} uses {len(names)} mappings; the device engine runs single-mapping loops"
+        )
+    return mesh.mappings[names[0]]
+
+
+def slot_mask(kernel, mesh, args) -> int:
+    mask = 0
+    for a in args:
+        for s in kernel.arg_slots(mesh, a):
+            mask |= 1 << int(s)
+    return mask
+
+
+# ---------------------------------------------------------------------------------
+# reorderings
+# ---------------------------------------------------------------------------------
+
+
+def point_graph(map_d: torch.Tensor, npts: int):
+    """Union of per-element cliques (reorder.py:63-79) as a device CSR."""
+    rows = map_d.long()
+    ar = rows.shape[1]
+    us, vs = [], []
+    for a in range(ar):
+        for b in range(a + 1, ar):
+            u, v = rows[:, a], rows[:, b]
+            keep = u != v
+            us.append(u[keep])
+            vs.append(v[keep])
+    if us:
+        u = torch.cat(us)
+        v = torch.cat(vs)
+        keys = torch.unique(torch.cat([u * npts + v, v * npts + u]))
+    else:
+        keys = torch.empty(0, dtype=torch.long, device=map_d.device)
+    src = torch.div(keys, npts, rounding_mode="floor")
+    dst = keys - src * npts
+    indptr = torch.zeros(npts + 1, dtype=torch.long, device=map_d.device)
+    if keys.numel():
+        indptr[1:] = torch.cumsum(torch.bincount(src, minlength=npts), 0)
+    return indptr, dst.to(torch.int32)
+
+
+def bfs(indptr, indices, start: int, levels: torch.Tensor) -> tuple:
+    n = indptr.numel() - 1
+    ecc = np.zeros(1, dtype=np.int32)
+    vis = np.zeros(1, dtype=np.int32)
+    _native.call("mp_bfs_levels", n, _native.ptr(indptr), _native.ptr(indices), int(start), _native.ptr(levels),
+                 ecc.ctypes.data, vis.ctypes.data, _sp())
+    return int(ecc[0]), int(vis[0])
+
+
+def gps_forward(map_d: torch.Tensor, npts: int) -> torch.Tensor:
+    """Forward point permutation of gps_renumber (reorder.py:115-141)."""
+    dev = map_d.device
+    indptr, indices = point_graph(map_d, npts)
+    deg = indptr[1:] - indptr[:-1]
+    comp = torch.arange(npts, dtype=torch.long, device=dev)  # component min id (singletons: self)
+    level = torch.zeros(npts, dtype=torch.long, device=dev)
+    assigned = deg == 0
+    lv = torch.empty(npts, dtype=torch.int32, device=dev)
+    ids = torch.arange(npts, dtype=torch.long, device=dev)
+    big = torch.iinfo(torch.long).max
+    while True:
+        free = torch.nonzero(~assigned)
+        if free.numel() == 0:
+            break
+        start = int(free[0, 0])
+        bfs(indptr, indices, start, lv)
+        in_comp = lv >= 0
+        cmin = start  # BFS from the lowest unassigned index: it is the component minimum
+        # pseudo-peripheral root (reorder.py:95-112): min (deg, id) start, then
+        # farthest-level min (deg, id) while the eccentricity grows
+        key = torch.where(in_comp, deg * npts + ids, torch.full_like(ids, big))
+        u = int(torch.argmin(key))
+        ecc, _ = bfs(indptr, indices, u, lv)
+        best = lv.clone()
+        while True:
+            last = best == ecc
+            key = torch.where(last, deg * npts + ids, torch.full_like(ids, big))
+            v = int(torch.argmin(key))
+            ecc_v, _ = bfs(indptr, indices, v, lv)
+            if ecc_v > ecc:
+                u, ecc, best = v, ecc_v, lv.clone()
+            else:
+                break
+        comp[in_comp] = cmin
+        level[in_comp] = best[in_comp].long()
+        assigned |= in_comp
+    # order by (component min, level, degree, id): stable LSD passes
+    order = ids
+    for k in (deg, level, comp):
+        _, idx = torch.sort(k[order], stable=True)
+        order = order[idx]
+    fwd = torch.empty(npts, dtype=torch.long, device=dev)
+    fwd[order] = ids
+    return fwd
+
+
+def lex_order(map_d: torch.Tensor, point_fwd: torch.Tensor, npts: int) -> torch.Tensor:
+    """Element order of lex_sort_elements (reorder.py:161-171): stable lexsort of
+    the sorted renumbered point tuples."""
+    keys, _ = torch.sort(point_fwd[map_d.long()], dim=1)
+    n, ar = keys.shape
+    order = torch.arange(n, dtype=torch.long, device=map_d.device)
+    col = ar - 1
+    while col >= 0:  # pack two columns per stable pass (npts < 2**31)
+        if col >= 1:
+            k = keys[:, col - 1] * npts + keys[:, col]
+            col -= 2
+        else:
+            k = keys[:, col]
+            col -= 1
+        _, idx = torch.sort(k[order], stable=True)
+        order = order[idx]
+    return order
+
+
+# ---------------------------------------------------------------------------------
+# block-level products
+# ---------------------------------------------------------------------------------
+
+
+def block_points(block_offsets_d, map_d, mask: int, max_block: int):
+    """Ascending unique points per block through the masked slots: int32 CSR."""
+    nb = block_offsets_d.numel() - 1
+    n, ar = map_d.shape
+    counts = torch.empty(max(nb, 1), dtype=torch.int32, device=map_d.device)
+    off = torch.zeros(nb + 1, dtype=torch.int32, device=map_d.device)
+    if nb == 0 or mask == 0:
+        return off, torch.empty(0, dtype=torch.int32, device=map_d.device)
+    args = (nb, _native.ptr(block_offsets_d), _native.ptr(map_d), n, ar, _native.MP_AOS, mask, int(max_block))
+    _native.call("mp_plan_block_points", *args, _native.ptr(counts), None, None, _sp())
+    off[1:] = torch.cumsum(counts[:nb], 0, dtype=torch.int32)
+    total = int(off[-1])
+    ids = torch.empty(max(total, 1), dtype=torch.int32, device=map_d.device)
+    _native.call("mp_plan_block_points", *args, _native.ptr(counts), _native.ptr(off), _native.ptr(ids), _sp())
+    return off, ids[:total]
+
+
+def thread_colours(block_offsets_d, map_d, written_mask: int, max_block: int):
+    """Per-block smallest-last/first-fit colours, counts and the stable colour sort."""
+    nb = block_offsets_d.numel() - 1
+    n, ar = map_d.shape
+    dev = map_d.device
+    cols = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+    counts = torch.zeros(max(nb, 1), dtype=torch.int32, device=dev)
+    order = torch.arange(max(n, 1), dtype=torch.int32, device=dev)
+    if nb and n:
+        _native.call("mp_plan_thread_colours", nb, _native.ptr(block_offsets_d), _native.ptr(map_d), n, ar,
+                     _native.MP_AOS, written_mask, int(max_block), _native.ptr(cols), _native.ptr(counts),
+                     _native.ptr(order), _sp())
+    return cols[:n], counts[:nb], order[:n]
+
+
+def local_slots(block_offsets_d, map_d, mask, st_off, st_ids, wr_off, wr_ids):
+    nb = block_offsets_d.numel() - 1
+    n, ar = map_d.shape
+    dev = map_d.device
+    ls = torch.full((max(n * ar, 1),), -1, dtype=torch.int16, device=dev)
+    ws = torch.full((max(wr_ids.numel(), 1),), -1, dtype=torch.int16, device=dev)
+    if nb:
+        _native.call("mp_plan_local_slots", nb, _native.ptr(block_offsets_d), _native.ptr(map_d), n, ar,
+                     _native.MP_AOS, mask, _native.ptr(st_off), _native.ptr(st_ids), _native.ptr(ls),
+                     _native.ptr(wr_off), _native.ptr(wr_ids), _native.ptr(ws), _sp())
+    return ls, ws
+
+
+def block_dag(wr_off, wr_ids, npts: int, block_colours_d, ncol: int):
+    """Predecessor lists (lower-colour blocks sharing a written point) and a
+    topological block order close to id order, for the dataflow schedule."""
+    nb = wr_off.numel() - 1
+    dev = wr_off.device
+    pred_off = torch.zeros(nb + 1, dtype=torch.int32, device=dev)
+    order = torch.arange(max(nb, 1), dtype=torch.int32, device=dev)
+    if nb == 0:
+        return pred_off, torch.zeros(1, dtype=torch.int32, device=dev), order[:0]
+    cap = 16 * nb + 1024
+    while True:
+        preds = torch.zeros(cap, dtype=torch.int32, device=dev)
+        npred = np.zeros(1, dtype=np.int64)
+        _native.call("mp_plan_block_dag", nb, _native.ptr(wr_off), _native.ptr(wr_ids), int(npts),
+                     _native.ptr(block_colours_d), int(ncol), _native.ptr(pred_off), _native.ptr(preds), cap,
+                     npred.ctypes.data, _native.ptr(order), _sp())
+        if int(npred[0]) <= cap:
+            return pred_off, preds[: max(int(npred[0]), 1)], order[:nb]
+        cap = int(npred[0])
+
+
+def split_oversized(offsets: np.ndarray, limit: int) -> np.ndarray:
+    """plan._split_oversized (451-464): halve any span wider than limit at
+    lo + (hi-lo+1)//2, depth first; only oversized spans are touched."""
+    sizes = np.diff(offsets)
+    if sizes.size == 0 or sizes.max() <= limit:
+        return offsets.astype(np.int64)
+    out = [int(offsets[0])]
+    big = set(np.flatnonzero(sizes > limit).tolist())
+    for b in range(sizes.size):
+        end = int(offsets[b + 1])
+        if b not in big:
+            out.append(end)
+            continue
+        pending = [(out[-1], end)]
+        while pending:
+            lo, hi = pending.pop(0)
+            if hi - lo > limit:
+                mid = lo + (hi - lo + 1) // 2
+                pending = [(lo, mid), (mid, hi)] + pending
+            else:
+                out.append(hi)
+    return np.asarray(out, dtype=np.int64)
+
+
+@dataclass
+class DevicePlan:
+    """Device-resident execution structures of one hierarchical plan."""
+
+    map: torch.Tensor               # (n, arity) int32, plan numbering
+    block_offsets: torch.Tensor     # int32 [nb+1]
+    staged_off: torch.Tensor
+    staged_ids: torch.Tensor
+    written_off: torch.Tensor
+    written_ids: torch.Tensor
+    written_slots: torch.Tensor     # int16 (uint16 bits)
+    local_slots: torch.Tensor       # int16 [n*arity]
+    thread_colours: torch.Tensor    # uint8 [n]
+    colour_counts: torch.Tensor     # int32 [nb]
+    blocks_by_colour: torch.Tensor  # int32 [nb]
+    colour_block_offsets: np.ndarray  # host int32 [ncol+1]
+    order: torch.Tensor             # int32 [nb]
+    pred_off: torch.Tensor
+    preds: torch.Tensor
+    flags: torch.Tensor             # int32 [nb] epoch stamps
+    tickets: torch.Tensor           # int32 [2]
+    block_size: int
+    max_staged: int
+    stage_reads: bool
+    epoch: int = 0
+
+    def struct(self) -> "_native.MpHierPlan":
+        p = _native.MpHierPlan()
+        p.num_blocks = self.block_offsets.numel() - 1
+        p.block_size = int(self.block_size)
+        p.stage_reads = int(self.stage_reads)
+        p.max_staged = int(self.max_staged)
+        for name, t in (("block_offsets", self.block_offsets), ("staged_offsets", self.staged_off),
+                        ("staged_ids", self.staged_ids), ("written_offsets", self.written_off),
+                        ("written_ids", self.written_ids), ("written_slots", self.written_slots),
+                        ("local_slots", self.local_slots), ("thread_colours", self.thread_colours),
+                        ("colour_counts", self.colour_counts), ("blocks_by_colour", self.blocks_by_colour),
+                        ("order", self.order), ("pred_offsets", self.pred_off), ("preds", self.preds),
+                        ("flags", self.flags), ("tickets", self.tickets)):
+            setattr(p, name, t.data_ptr())
+        p.num_block_colours = len(self.colour_block_offsets) - 1
+        p.colour_block_offsets_host = self.colour_block_offsets.ctypes.data
+        return p
+
+
+def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sorted_d, tcounts_d, st_off, st_ids,
+                      wr_off, wr_ids, stage_mask, stage_reads, npts, block_size) -> DevicePlan:
+    """Assemble the executor structures (slots, schedules) from plan arrays."""
+    dev = map_d.device
+    bo = torch.as_tensor(block_offsets_np.astype(np.int32), device=dev)
+    nb = bo.numel() - 1
+    ls, ws = local_slots(bo, map_d, stage_mask, st_off, st_ids, wr_off, wr_ids)
+    bc = torch.as_tensor(block_colours_np.astype(np.int32), device=dev)
+    by_colour = np.lexsort((np.arange(nb), block_colours_np)).astype(np.int32) if nb else np.zeros(0, np.int32)
+    cbo = np.zeros(ncol + 1, dtype=np.int32)
+    if nb:
+        cbo[1:] = np.cumsum(np.bincount(block_colours_np, minlength=ncol))
+    pred_off, preds, order = block_dag(wr_off, wr_ids, npts, bc, ncol)
+    counts = np.diff(st_off.cpu().numpy()) if nb else np.zeros(0)
+    if tcounts_d.numel() and int(tcounts_d.max()) > 255:
+        raise CapacityError("a block needs more than 255 thread colours")
+    return DevicePlan(
+        map=map_d, block_offsets=bo, staged_off=st_off, staged_ids=st_ids, written_off=wr_off, written_ids=wr_ids,
+        written_slots=ws, local_slots=ls, thread_colours=tcol_sorted_d.to(torch.uint8),
+        colour_counts=tcounts_d.to(torch.int32), blocks_by_colour=torch.as_tensor(by_colour, device=dev),
+        colour_block_offsets=cbo, order=order, pred_off=pred_off, preds=preds,
+        flags=torch.zeros(max(nb, 1), dtype=torch.int32, device=dev),
+        tickets=torch.zeros(2, dtype=torch.int32, device=dev),
+        block_size=int(block_size), max_staged=int(counts.max()) if counts.size else 0, stage_reads=bool(stage_reads),
+    )
+
+
+def check_block_widths(offsets: np.ndarray, limit: int) -> None:
+    if offsets.size > 1 and int(np.diff(offsets).max()) > limit:
+        raise CapacityError("plan contains a block wider than the configured block size")
+
+
+def to_host_i64(t: torch.Tensor) -> np.ndarray:
+    return t.to(torch.int64).cpu().numpy()
+
+
+def validate_device_limits(mesh: Mesh, m: Mapping | None) -> None:
+    for s in mesh.sets.values():
+        if s.size >= 2**31 - 1:
+            raise MeshValidationError(f"set {s.name!r} too large for int32 device indices")
+    if m is not None and m.arity > 32:
+        raise KernelSpecError(f"mapping {m.name!r} arity {m.arity} exceeds the device limit of 32")
