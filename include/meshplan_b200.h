@@ -99,7 +99,8 @@ typedef struct mp_hier_plan {
   const int32_t* pred_offsets;    /* [nb+1]                                  */
   const int32_t* preds;           /* conflicting blocks of lower colour      */
   uint32_t* flags;                /* [nb] epoch stamps, zero-initialised     */
-  uint32_t* tickets;              /* [2] ticket counters, zero-initialised   */
+  uint32_t* tickets;              /* [2] next-block ticket, finished blocks;
+                                     zero-initialised, re-armed by the kernel */
 } mp_hier_plan;
 
 /* ---- library ------------------------------------------------------------ */
@@ -127,6 +128,15 @@ mp_status mp_exec_hier(const mp_loop* loop, const mp_hier_plan* plan, int32_t sc
  * np.add.at order.  temp must hold n_elems*arity*inc_comps elements. */
 mp_status mp_exec_serial(const mp_loop* loop, const int32_t* inv_offsets, const int32_t* inv_refs, void* temp,
                          void* stream);
+
+/* ---- multi-GPU halo (owner compute; no reference counterpart) ----- */
+/* dst[r*comps + c] = src[rows[r]*comps + c]  (pack rows a peer imports)      */
+mp_status mp_halo_pack(int32_t dtype, const void* src, const int32_t* rows, int64_t nrows, int32_t comps, void* dst,
+                       void* stream);
+/* dst[rows[r]*comps + c] = src[r*comps + c] (mode 0), += (mode 1, fold a peer's
+ * increments), = 0 (mode 2, re-zero halo increments); rows distinct */
+mp_status mp_halo_unpack(int32_t dtype, void* dst, const int32_t* rows, int64_t nrows, int32_t comps,
+                         const void* src, int32_t mode, void* stream);
 
 /* ---- race checks (simulator.py:245-261, 446-469) ---------------------------- */
 /* Keys (group*key_span + point) over every (element, written point) ref;

@@ -58,8 +58,7 @@ __global__ void __launch_bounds__(1024) hier_block_kernel(LoopView<T> v, HierVie
   int b;
   if constexpr (DATAFLOW) {
     if (tid == 0) {
-      if (blockIdx.x == 0) H.tickets[(H.epoch + 1) & 1] = 0u;  // next launch's counter
-      uint32_t t = atomicAdd(&H.tickets[H.epoch & 1], 1u);
+      uint32_t t = atomicAdd(&H.tickets[0], 1u);  // tickets[0]: next block, tickets[1]: blocks done
       s_block = __ldg(H.order + t);
     }
     __syncthreads();
@@ -174,6 +173,12 @@ __global__ void __launch_bounds__(1024) hier_block_kernel(LoopView<T> v, HierVie
     if (tid == 0) {
       __threadfence();
       st_release_gpu(H.flags + b, H.epoch);
+      // the last block to finish re-arms the counters for the next launch
+      // (stream order makes the next launch see the reset)
+      if (atomicAdd(&H.tickets[1], 1u) == gridDim.x - 1) {
+        H.tickets[0] = 0u;
+        H.tickets[1] = 0u;
+      }
     }
   }
 }

@@ -1,0 +1,330 @@
+"""Owner-compute domain decomposition across GPUs.
+
+The reference is single-process; this is the new
+multi-GPU axis.  The to-set (cells) is split into contiguous owner ranges;
+every element goes to the owner of its first point.  A rank's local to-set
+is its owned points followed by its halo (points its elements touch but
+another rank owns), grouped by owner.  One loop step is
+
+  1. import halo of indirectly read data: each owner packs the rows a peer
+     imports (mp_halo_pack) and sends them; the importer scatters them into
+     its halo rows (mp_halo_unpack, set);
+  2. the local hierarchical loop (any plan / schedule) on the local mesh;
+  3. export halo increments: the importer packs its halo increment rows and
+     sends them to the owner, which folds them in (mp_halo_unpack, add); the
+     importer re-zeroes its halo rows (mp_halo_unpack, zero).
+
+Row lists are in the local *plan* numbering (a plan may renumber points,
+e.g. GPS), so nothing assumes contiguous halo rows.  Transports:
+``TorchDistTransport`` (torch.distributed send/recv: NCCL over NVLink on the
+GPU box, gloo on CPU in the tests) and ``ThreadTransport`` (in-process
+queues, to run N ranks on one GPU).  Per point, remote contributions are
+added after the owner's local loop, so results equal the serial loop exactly
+on the generators' 1/1024-grid data and within reassociation tolerance
+otherwise.
+"""
+
+import queue
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native
+
+TORCH_TO_MP = {torch.float64: _native.MP_F64, torch.float32: _native.MP_F32, torch.int64: _native.MP_I64,
+               torch.int32: _native.MP_I32}
+SET, ADD, ZERO = 0, 1, 2
+
+
+@dataclass
+class Decomposition:
+    rank: int
+    world: int
+    lo: int                       # owned global point range [lo, hi)
+    hi: int
+    local_points: np.ndarray      # global ids: owned (ascending) then halo (by owner, then id)
+    halo_rows: dict               # peer -> local rows of my halo owned by peer (ascending global id)
+    export_rows: dict             # peer -> local rows of my owned points in the peer's halo (same order)
+    local_table: np.ndarray       # (local elements, arity) local point ids
+    elem_ids: np.ndarray          # global element ids of the local elements
+
+    @property
+    def n_owned(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def n_local(self) -> int:
+        return int(self.local_points.size)
+
+    def renumbered(self, point_fwd: np.ndarray) -> "Decomposition":
+        """The same exchange expressed in a plan's point numbering."""
+        f = np.asarray(point_fwd)
+        return Decomposition(self.rank, self.world, self.lo, self.hi, self.local_points,
+                             {p: f[r] for p, r in self.halo_rows.items()},
+                             {p: f[r] for p, r in self.export_rows.items()}, self.local_table, self.elem_ids)
+
+
+def owner_of(points: np.ndarray, bounds: np.ndarray) -> np.ndarray:
+    return np.searchsorted(bounds, points, side="right") - 1
+
+
+def decompose(table: np.ndarray, elem_ids: np.ndarray, bounds, rank: int, world: int, allgather) -> Decomposition:
+    """Local numbering and exchange lists for this rank's elements.
+
+    ``table`` holds the rank's elements (global point ids); ``bounds`` the
+    owner ranges (world+1 ascending ids); ``allgather(obj)`` returns the list
+    of every rank's ``obj`` (a collective over all ranks)."""
+    bounds = np.asarray(bounds, dtype=np.int64)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    pts = np.unique(table)
+    halo_pts = pts[(pts < lo) | (pts >= hi)]
+    own = owner_of(halo_pts, bounds)
+    n_owned = hi - lo
+    halo_rows = {int(p): n_owned + np.flatnonzero(own == p) for p in np.unique(own).tolist()}
+    local_points = np.concatenate([np.arange(lo, hi, dtype=np.int64), halo_pts])
+    inside = (table >= lo) & (table < hi)
+    local_table = np.where(inside, table - lo, n_owned + np.searchsorted(halo_pts, table)).astype(np.int64)
+    everyone = allgather(halo_pts)
+    export_rows = {}
+    for peer, theirs in enumerate(everyone):
+        if peer == rank:
+            continue
+        theirs = np.asarray(theirs, dtype=np.int64)
+        mine = theirs[owner_of(theirs, bounds) == rank]
+        if mine.size:
+            export_rows[peer] = mine - lo
+    return Decomposition(rank, world, lo, hi, local_points, halo_rows, export_rows, local_table,
+                         np.asarray(elem_ids, dtype=np.int64))
+
+
+# ---- device pack / unpack (hand-written kernels; the CPU tests patch these) -----------
+
+
+def pack_rows(src: torch.Tensor, rows: torch.Tensor, comps: int, out: torch.Tensor) -> None:
+    _native.call("mp_halo_pack", TORCH_TO_MP[src.dtype], src.data_ptr(), rows.data_ptr(), rows.numel(), comps,
+                 out.data_ptr(), _native.stream_ptr())
+
+
+def unpack_rows(dst: torch.Tensor, rows: torch.Tensor, comps: int, src, mode: int) -> None:
+    _native.call("mp_halo_unpack", TORCH_TO_MP[dst.dtype], dst.data_ptr(), rows.data_ptr(), rows.numel(), comps,
+                 None if src is None else src.data_ptr(), mode, _native.stream_ptr())
+
+
+# ---- transports --------------------------------------------------------------------------
+
+
+class TorchDistTransport:
+    """Point-to-point exchange through torch.distributed (NCCL / gloo)."""
+
+    def exchange(self, send: dict, recv: dict) -> None:
+        import torch.distributed as dist
+
+        ops = [dist.P2POp(dist.isend, t, peer) for peer, t in sorted(send.items())]
+        ops += [dist.P2POp(dist.irecv, t, peer) for peer, t in sorted(recv.items())]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+
+@dataclass
+class ThreadHub:
+    """Mailboxes connecting the ThreadTransports of one process."""
+
+    boxes: dict = field(default_factory=dict)
+
+    def box(self, src, dst) -> queue.Queue:
+        return self.boxes.setdefault((src, dst), queue.Queue())
+
+
+class ThreadTransport:
+    """In-process transport: each simulated rank runs in its own thread."""
+
+    def __init__(self, hub: ThreadHub, rank: int):
+        self.hub, self.rank = hub, rank
+
+    def exchange(self, send: dict, recv: dict) -> None:
+        if any(t.is_cuda for t in send.values()):
+            torch.cuda.current_stream().synchronize()
+        for peer, t in send.items():
+            self.hub.box(self.rank, peer).put(t.clone())
+        for peer, t in recv.items():
+            t.copy_(self.hub.box(peer, self.rank).get())
+
+
+class HaloExchange:
+    """Halo import of a read array and export of an increment array (AoS rows,
+    flat tensors of rows*comps values)."""
+
+    def __init__(self, dec: Decomposition, transport, device):
+        self.dec, self.tr, self.dev = dec, transport, torch.device(device)
+        as_rows = lambda r: torch.as_tensor(np.asarray(r, dtype=np.int32), device=self.dev)  # noqa: E731
+        self.halo = {p: as_rows(r) for p, r in dec.halo_rows.items()}
+        self.exports = {p: as_rows(r) for p, r in dec.export_rows.items()}
+        self.all_halo = as_rows(np.concatenate(list(dec.halo_rows.values()))) if dec.halo_rows else None
+        self._bufs = {}
+
+    def _buf(self, key, n, dtype):
+        b = self._bufs.get(key)
+        if b is None or b.numel() != n or b.dtype != dtype:
+            b = torch.empty(n, dtype=dtype, device=self.dev)
+            self._bufs[key] = b
+        return b
+
+    def import_rows(self, arr: torch.Tensor, comps: int) -> None:
+        send, recv = {}, {}
+        for peer, rows in self.exports.items():
+            send[peer] = self._buf(("is", peer, comps), rows.numel() * comps, arr.dtype)
+            pack_rows(arr, rows, comps, send[peer])
+        for peer, rows in self.halo.items():
+            recv[peer] = self._buf(("ir", peer, comps), rows.numel() * comps, arr.dtype)
+        self.tr.exchange(send, recv)
+        for peer, rows in self.halo.items():
+            unpack_rows(arr, rows, comps, recv[peer], SET)
+
+    def export_increments(self, arr: torch.Tensor, comps: int) -> None:
+        send, recv = {}, {}
+        for peer, rows in self.halo.items():
+            send[peer] = self._buf(("es", peer, comps), rows.numel() * comps, arr.dtype)
+            pack_rows(arr, rows, comps, send[peer])
+        for peer, rows in self.exports.items():
+            recv[peer] = self._buf(("er", peer, comps), rows.numel() * comps, arr.dtype)
+        self.tr.exchange(send, recv)
+        for peer, rows in self.exports.items():
+            unpack_rows(arr, rows, comps, recv[peer], ADD)
+        if self.all_halo is not None:
+            unpack_rows(arr, self.all_halo, comps, None, ZERO)
+
+    def launches_per_step(self) -> int:
+        return 2 * (len(self.halo) + len(self.exports)) + (1 if self.all_halo is not None else 0)
+
+
+def slab_bounds(nx: int, ny: int, world: int):
+    """Owner ranges of a quad2d mesh cut into x-slabs (cell = x*ny + y)."""
+    xs = np.array([(r * nx) // world for r in range(world + 1)], dtype=np.int64)
+    return xs * ny, xs
+
+
+# ---- a decomposed loop -----------------------------------------------------------------
+
+
+class DistributedLoop:
+    """One rank's share of a decomposed flux-type loop: local plan + halo."""
+
+    def __init__(self, mesh_local, kernel, dec: Decomposition, transport, config, schedule="dataflow"):
+        import paper_1802_03749_b200 as mp
+
+        self.plan = mp.build_hierarchical_plan(mesh_local, kernel, config)
+        self.loop = mp.bind(self.plan, kernel, schedule=schedule)
+        cells = next(iter(mesh_local.mappings.values())).to_set.name
+        self.dec = dec.renumbered(self.plan.set_perms[cells].forward)
+        self.halo = HaloExchange(self.dec, transport, "cuda")
+        self.read = next((a.array for a in kernel.indirect_read_args), None)
+        self.inc = kernel.increment_args[0].array
+        self.rc = None if self.read is None else mesh_local.data[self.read].components
+        self.ic = mesh_local.data[self.inc].components
+
+    def step(self) -> None:
+        if self.read is not None:
+            self.halo.import_rows(self.loop.tensors[self.read], self.rc)
+        self.loop.run()
+        self.halo.export_increments(self.loop.tensors[self.inc], self.ic)
+
+    def owned_result(self) -> np.ndarray:
+        """Owned rows of the increment array, in the decomposition's (global) order."""
+        pf = self.plan.set_perms[next(iter(self.plan.mesh.mappings.values())).to_set.name].forward
+        v = self.loop.tensors[self.inc].reshape(-1, self.ic).cpu().numpy()
+        return v[pf[: self.dec.n_owned]]
+
+    def launches_per_step(self) -> int:
+        return self.loop.launches_per_run() + self.halo.launches_per_step()
+
+
+def local_flux_mesh(table, elem_ids, dec: Decomposition, q_global_rows, w_rows, res_rows):
+    """Local mesh of a rank from its element rows and point rows (AoS f64)."""
+    import paper_1802_03749_b200 as mp
+
+    edges, cells = mp.MeshSet("edges", table.shape[0]), mp.MeshSet("cells", dec.n_local)
+    data = [mp.DataArray("q", cells, 4, np.ascontiguousarray(q_global_rows).reshape(-1)),
+            mp.DataArray("res", cells, 4, np.ascontiguousarray(res_rows).reshape(-1)),
+            mp.DataArray("w", edges, 2, np.ascontiguousarray(w_rows).reshape(-1))]
+    return mp.Mesh.build([edges, cells], [mp.Mapping("e2c", edges, cells, dec.local_table)], data)
+
+
+# ---- benchmark rank (bench.py --gpus N under torchrun) -----------------------------------
+
+
+def bench_rank(args, rank: int, world: int) -> int:
+    import json
+    import os
+    import time
+
+    import torch.distributed as dist
+
+    import paper_1802_03749_b200 as mp
+    from .workloads import hashed_grid_values, quad2d_table
+
+    bench = __import__("bench")
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist.init_process_group("nccl", device_id=dev)
+    family, dims, kname, dtype, staging = bench.CONFIGS[args.config]
+    if family != "quad2d" or kname != "flux":
+        raise SystemExit("the multi-GPU bench decomposes the quad2d flux configs (C1/C5)")
+    nx, ny = dims
+    bounds, xs = slab_bounds(nx, ny, world)
+    t0 = time.perf_counter()
+    table, gids = quad2d_table(nx, ny, int(xs[rank]), int(xs[rank + 1]))
+
+    def allgather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    dec = decompose(table, gids, bounds, rank, world, allgather)
+    cid = torch.as_tensor(dec.local_points, device=dev)
+    q = hashed_grid_values(cid[:, None] * 4 + torch.arange(4, device=dev), 0, 1).cpu().numpy()
+    g = torch.as_tensor(gids, device=dev)
+    w = hashed_grid_values(g[:, None] * 2 + torch.arange(2, device=dev), 0, 3).cpu().numpy()
+    mesh = local_flux_mesh(table, gids, dec, q, w, np.zeros((dec.n_local, 4)))
+    kernel = mp.kernel_for_mesh("flux", mesh)
+    cfg = mp.PlanConfig(reorder=args.reorder, layout="aos", block_size=args.block_size)
+    dl = DistributedLoop(mesh, kernel, dec, TorchDistTransport(), cfg, args.schedule)
+    t_plan = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        dl.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        dl.step()
+    b.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    n_edges = nx * (ny - 1) + ny * (nx - 1)
+    ub_total = nx * ny * 4 * 8 * 3 + n_edges * (2 * 8 + 2 * 4)
+    peak, kind = bench.hbm_peak()
+    gbps = ub_total / (float(ms) * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": bench.METRIC, "value": round(gbps, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(float(ms), 5),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": f"{args.config}: quad2d {nx}x{ny} flux f64 decomposed into {world} x-slabs",
+                       "strategy": "hier", "reorder": args.reorder, "schedule": args.schedule,
+                       "parallelism": f"owner-compute x{world}, NCCL halo exchange",
+                       "useful_bytes_per_step": ub_total, "l2": "inputs larger than L2 (no flush)"},
+            "roofline": {"bound": "hbm", "achieved": round(gbps / world, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbps / world / peak, 4), "traffic": None, "peak_kind": kind,
+                         "note": "per-GPU share of the whole-job effective bandwidth"},
+            "gpu_launches": int(args.steps * dl.launches_per_step()),
+            "cpu_baseline": None, "plan_build_s": round(t_plan, 2),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0

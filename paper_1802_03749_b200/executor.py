@@ -165,8 +165,9 @@ class DeviceLoop:
             _native.call("mp_exec_global", self.loop, offs.ctypes.data, len(offs) - 1,
                          int(self.plan.config.block_size), sp)
         else:
-            dp.epoch += 1
-            _native.call("mp_exec_hier", self.loop, dp.struct_cached(), self.schedule, dp.epoch & 0xFFFFFFFF, sp)
+            if self.schedule == _native.MP_SCHED_DATAFLOW:
+                dp.epoch = dp.epoch % 0xFFFFFFFF + 1  # flags hold the last epoch; never 0
+            _native.call("mp_exec_hier", self.loop, dp.struct_cached(), self.schedule, max(dp.epoch, 1), sp)
 
     def run_host(self, inputs: dict, out, stream=None) -> None:
         """One end-to-end step with host buffers: H2D of the given arrays

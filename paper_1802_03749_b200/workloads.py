@@ -221,7 +221,9 @@ def hashed_grid_values(index, seed: int, salt: int):
         x = x ^ (x >> 16)
         x = (x * 0x45D9F3B) & mask
     x = x ^ (x >> 16)
-    return ((x % 2049) - 1024) / 1024.0
+    v = (x % 2049) - 1024
+    v = v.to(__import__("torch").float64) if hasattr(v, "to") else v.astype(np.float64)
+    return v / 1024.0
 
 
 def quad2d_table(nx: int, ny: int, xlo: int = 0, xhi: int | None = None):
