@@ -183,6 +183,22 @@ mp_status mp_greedy_colour_adj(int64_t n, const int64_t* indptr, const int64_t* 
 /* Smallest-last elimination order (numpy_impl.py:95-111), host C++. */
 mp_status mp_smallest_last_order(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t* order);
 
+/* Multilevel k-way partitioner pieces (partition.py:173-350), host C++,
+ * bit-identical to the reference's sequential sweeps.  CSR graphs are int64
+ * host arrays; `assignment` / `block_w` are updated in place. */
+mp_status mp_heavy_edge_matching(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
+                                 const int64_t* node_w, const int64_t* visit, int64_t max_cluster, int64_t* match);
+mp_status mp_cut_weight(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
+                        const int64_t* assignment, int32_t use_w, int64_t* cut);
+mp_status mp_refine_boundary_pass(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
+                                  int64_t* assignment, int64_t* block_w, int64_t num_blocks, const int64_t* node_w,
+                                  int64_t cap, int32_t use_w, int64_t* moves);
+mp_status mp_rebalance(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
+                       int64_t* assignment, int64_t* block_w, int64_t num_blocks, const int64_t* node_w, int64_t cap,
+                       int32_t use_w);
+mp_status mp_initial_partition(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* node_w,
+                               int64_t num_blocks, int64_t cap, int64_t* assignment);
+
 /* Level-synchronous BFS on a device CSR graph (numpy_impl.py:114-131):
  * levels[v] (-1 unreached); returns the eccentricity and visited count.
  * Levels are independent of visit order, so equal to the reference. */

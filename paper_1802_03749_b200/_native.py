@@ -67,7 +67,12 @@ _SIGNATURES = {
     "mp_smallest_last_order": (c_i32, [c_i64, c_vp, c_vp, c_vp]),
     "mp_bfs_levels": (c_i32, [c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "mp_plan_block_dag": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
-    "mp_halo_pack": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "mp_heavy_edge_matching": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "mp_cut_weight": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "mp_refine_boundary_pass": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_vp]),
+    "mp_rebalance": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32]),
+    "mp_initial_partition": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]),
+    "mp_halo_pack":(c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "mp_halo_unpack": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp]),
     "mp_free": (None, [c_vp]),
 }

@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <limits>
 #include <set>
 #include <utility>
@@ -153,6 +154,226 @@ extern "C" mp_status mp_smallest_last_order(int64_t n, const int64_t* indptr, co
       deg[v]--;
       live.insert({deg[v], v});
     }
+  }
+  return MP_OK;
+}
+
+// ---- multilevel k-way partitioner pieces (partition.py:173-350) -------------------------
+
+// numpy_impl.py:134-157 -- greedy heavy-edge matching in a given visit order.
+extern "C" mp_status mp_heavy_edge_matching(int64_t n, const int64_t* indptr, const int64_t* indices,
+                                            const int64_t* weights, const int64_t* node_w, const int64_t* visit,
+                                            int64_t max_cluster, int64_t* match) {
+  mp::clear_error();
+  for (int64_t u = 0; u < n; ++u) match[u] = -1;
+  for (int64_t step = 0; step < n; ++step) {
+    const int64_t u = visit[step];
+    if (match[u] >= 0) continue;
+    int64_t best = u, best_w = -1;
+    for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) {
+      const int64_t v = indices[j];
+      if (match[v] >= 0 || v == u) continue;
+      if (node_w[u] + node_w[v] > max_cluster) continue;
+      const int64_t w = weights[j];
+      if (w > best_w || (w == best_w && v < best)) {
+        best = v;
+        best_w = w;
+      }
+    }
+    match[u] = best;
+    if (best != u) match[best] = u;
+  }
+  return MP_OK;
+}
+
+// numpy_impl.py:197-206
+extern "C" mp_status mp_cut_weight(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
+                                   const int64_t* assignment, int32_t use_w, int64_t* cut) {
+  mp::clear_error();
+  int64_t c = 0;
+  for (int64_t u = 0; u < n; ++u)
+    for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) {
+      const int64_t v = indices[j];
+      if (u < v && assignment[u] != assignment[v]) c += use_w ? weights[j] : 1;
+    }
+  *cut = c;
+  return MP_OK;
+}
+
+// numpy_impl.py:160-194 -- one in-place boundary refinement sweep.
+extern "C" mp_status mp_refine_boundary_pass(int64_t n, const int64_t* indptr, const int64_t* indices,
+                                             const int64_t* weights, int64_t* assignment, int64_t* block_w,
+                                             int64_t num_blocks, const int64_t* node_w, int64_t cap, int32_t use_w,
+                                             int64_t* moves_out) {
+  mp::clear_error();
+  std::vector<int64_t> conn(num_blocks, 0), touched(num_blocks);
+  int64_t moves = 0;
+  for (int64_t u = 0; u < n; ++u) {
+    const int64_t own = assignment[u];
+    int64_t nt = 0;
+    for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) {
+      const int64_t b = assignment[indices[j]];
+      if (conn[b] == 0) touched[nt++] = b;
+      conn[b] += use_w ? weights[j] : 1;
+    }
+    int64_t best = own, best_gain = 0;
+    for (int64_t k = 0; k < nt; ++k) {
+      const int64_t b = touched[k];
+      if (b == own) continue;
+      const int64_t gain = conn[b] - conn[own];
+      if (gain > best_gain || (gain == best_gain && best != own && b < best)) {
+        if (block_w[b] + node_w[u] <= cap && block_w[own] - node_w[u] > 0) {
+          best = b;
+          best_gain = gain;
+        }
+      }
+    }
+    if (best != own) {
+      assignment[u] = best;
+      block_w[own] -= node_w[u];
+      block_w[best] += node_w[u];
+      ++moves;
+    }
+    for (int64_t k = 0; k < nt; ++k) conn[touched[k]] = 0;
+  }
+  *moves_out = moves;
+  return MP_OK;
+}
+
+// partition.py:255-285 -- push members out of over-cap blocks (best effort).
+extern "C" mp_status mp_rebalance(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
+                                  int64_t* assignment, int64_t* block_w, int64_t num_blocks, const int64_t* node_w,
+                                  int64_t cap, int32_t use_w) {
+  mp::clear_error();
+  int64_t guard = 0;
+  std::vector<int64_t> conn(num_blocks), members;
+  while (true) {
+    int64_t b = -1;
+    for (int64_t k = 0; k < num_blocks; ++k)
+      if (block_w[k] > cap) {
+        b = k;
+        break;
+      }
+    if (b < 0 || guard > n * 4) break;
+    ++guard;
+    members.clear();
+    for (int64_t u = 0; u < n; ++u)
+      if (assignment[u] == b) members.push_back(u);
+    bool moved = false;
+    for (int64_t u : members) {
+      if (block_w[b] <= cap) break;
+      std::fill(conn.begin(), conn.end(), 0);
+      for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) conn[assignment[indices[j]]] += use_w ? weights[j] : 1;
+      conn[b] = -1;
+      // candidate with the largest connectivity, ties by lowest id, that has room
+      int64_t best = -1;
+      for (int64_t c = 0; c < num_blocks; ++c) {
+        if (c == b || block_w[c] + node_w[u] > cap) continue;
+        if (best < 0 || conn[c] > conn[best]) best = c;
+      }
+      if (best < 0) continue;
+      assignment[u] = best;
+      block_w[b] -= node_w[u];
+      block_w[best] += node_w[u];
+      moved = true;
+    }
+    if (!moved) break;
+  }
+  return MP_OK;
+}
+
+namespace {
+// partition.py:198-236 -- region-growing bisection of `subset` (ascending).
+void grow_bisection(const int64_t* indptr, const int64_t* indices, const int64_t* node_w,
+                    const std::vector<int64_t>& subset, int64_t k1, int64_t k2, int64_t cap, std::vector<char>& in_sub,
+                    std::vector<char>& taken, std::vector<int64_t>& left, std::vector<int64_t>& right) {
+  int64_t total = 0;
+  for (int64_t u : subset) total += node_w[u];
+  const int64_t lower = std::max<int64_t>(0, total - k2 * cap);
+  const int64_t upper = std::min<int64_t>(k1 * cap, total);
+  // Python: int(round(total * k1 / (k1 + k2))) -- true division, round half to even
+  const double q = (double)(total * k1) / (double)(k1 + k2);
+  int64_t target = (int64_t)std::nearbyint(q);
+  target = std::min(std::max(target, lower), upper);
+  for (int64_t u : subset) in_sub[u] = 1;
+  std::vector<int64_t> queue;
+  queue.reserve(subset.size());
+  left.clear();
+  int64_t w = 0;
+  size_t seed_pos = 0, head = 0;
+  while (w < target) {
+    if (head >= queue.size()) {
+      while (seed_pos < subset.size() && taken[subset[seed_pos]]) ++seed_pos;
+      if (seed_pos >= subset.size()) break;
+      queue.push_back(subset[seed_pos]);
+      taken[subset[seed_pos]] = 1;
+    }
+    const int64_t u = queue[head++];
+    if (w + node_w[u] > upper) continue;
+    left.push_back(u);
+    w += node_w[u];
+    for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) {
+      const int64_t v = indices[j];
+      if (in_sub[v] && !taken[v]) {
+        taken[v] = 1;
+        queue.push_back(v);
+      }
+    }
+  }
+  std::sort(left.begin(), left.end());
+  // right = subset minus left, subset order
+  right.clear();
+  std::vector<int64_t>::const_iterator it = left.begin();
+  for (int64_t u : subset) {
+    while (it != left.end() && *it < u) ++it;
+    if (it != left.end() && *it == u) continue;
+    right.push_back(u);
+  }
+  for (int64_t u : subset) {
+    in_sub[u] = 0;
+    taken[u] = 0;
+  }
+  for (int64_t u : queue) taken[u] = 0;
+}
+}  // namespace
+
+// partition.py:239-252 -- recursive bisection seeding of num_blocks blocks.
+extern "C" mp_status mp_initial_partition(int64_t n, const int64_t* indptr, const int64_t* indices,
+                                          const int64_t* node_w, int64_t num_blocks, int64_t cap,
+                                          int64_t* assignment) {
+  mp::clear_error();
+  for (int64_t u = 0; u < n; ++u) assignment[u] = -1;
+  std::vector<char> in_sub(n, 0), taken(n, 0);
+  struct Job {
+    std::vector<int64_t> subset;
+    int64_t first, k;
+  };
+  std::vector<Job> stack;
+  Job root;
+  root.subset.resize(n);
+  for (int64_t u = 0; u < n; ++u) root.subset[u] = u;
+  root.first = 0;
+  root.k = num_blocks;
+  stack.push_back(std::move(root));
+  std::vector<int64_t> left, right;
+  while (!stack.empty()) {
+    Job job = std::move(stack.back());
+    stack.pop_back();
+    if (job.k == 1 || job.subset.empty()) {
+      for (int64_t u : job.subset) assignment[u] = job.first;
+      continue;
+    }
+    const int64_t k1 = (job.k + 1) / 2;
+    grow_bisection(indptr, indices, node_w, job.subset, k1, job.k - k1, cap, in_sub, taken, left, right);
+    Job a, b;
+    a.subset = left;
+    a.first = job.first;
+    a.k = k1;
+    b.subset = right;
+    b.first = job.first + k1;
+    b.k = job.k - k1;
+    stack.push_back(std::move(b));
+    stack.push_back(std::move(a));
   }
   return MP_OK;
 }

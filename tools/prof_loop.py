@@ -1,0 +1,53 @@
+"""Profiling driver: build one plan, then run the loop a few times (for ncu).
+
+    python tools/prof_loop.py --config C5 --strategy hier --schedule colour --runs 3
+"""
+
+import argparse
+import sys
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(REPO))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--strategy", default="hier", choices=("hier", "global"))
+    ap.add_argument("--schedule", default="colour")
+    ap.add_argument("--reorder", default="gps")
+    ap.add_argument("--layout", default="aos")
+    ap.add_argument("--block-size", type=int, default=128)
+    ap.add_argument("--runs", type=int, default=3)
+    args = ap.parse_args()
+
+    import torch
+
+    import bench
+    import paper_1802_03749_b200 as mp
+
+    mesh, kernel, staging = bench.make_mesh(args.config)
+    cfg = mp.PlanConfig(strategy=args.strategy, reorder=args.reorder, layout=args.layout, staging=staging,
+                        block_size=args.block_size)
+    t0 = time.perf_counter()
+    plan = (mp.build_global_plan if args.strategy == "global" else mp.build_hierarchical_plan)(mesh, kernel, cfg)
+    print(f"plan {time.perf_counter() - t0:.2f}s", flush=True)
+    loop = mp.bind(plan, kernel, schedule=args.schedule)
+    torch.cuda.synchronize()
+    for _ in range(args.runs):
+        loop.run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    loop.run()
+    b.record()
+    torch.cuda.synchronize()
+    ub = mp.useful_bytes(kernel, mesh)
+    ms = a.elapsed_time(b)
+    print(f"{args.strategy}/{args.schedule}: {ms:.4f} ms  {ub / ms / 1e6:.1f} GB/s", flush=True)
+
+
+if __name__ == "__main__":
+    main()
