@@ -79,13 +79,15 @@ typedef struct mp_hier_plan {
   int32_t block_size;           /* widest block (CTA width)                 */
   int32_t stage_reads;          /* 1: all-indirect staging, 0: increment-only */
   int32_t max_staged;           /* widest staged list (shared sizing)        */
-  const int32_t* block_offsets;   /* [nb+1]                                  */
-  const int32_t* staged_offsets;  /* [nb+1]                                  */
+  int32_t slot_bytes;           /* 1 (max_staged <= 256) or 2: local_slots width */
+  int32_t written_is_staged;    /* 1: every block's written list == staged list */
+  const int32_t* meta;            /* [nb][4] {first element, elements,
+                                     staged offset, staged count}            */
   const int32_t* staged_ids;      /* ascending per block                     */
-  const int32_t* written_offsets; /* [nb+1]                                  */
+  const int32_t* written_offsets; /* [nb+1] (written_is_staged == 0 only)    */
   const int32_t* written_ids;     /* ascending per block                     */
   const uint16_t* written_slots;  /* staged slot of each written entry       */
-  const uint16_t* local_slots;    /* [n_elems*arity] staged slot per map entry */
+  const void* local_slots;        /* [n_elems*arity] staged slot per map entry */
   const uint8_t* thread_colours;  /* [n_elems] sorted within each block      */
   const int32_t* colour_counts;   /* [nb] thread colours per block           */
   /* MP_SCHED_COLOUR: one launch per block colour */
@@ -210,7 +212,7 @@ mp_status mp_bfs_levels(int32_t n, const int64_t* indptr, const int32_t* indices
  * (colour, id); order = blocks sorted by (key, id) where
  * key(b) = max(b, max_pred key+1), a topological order close to id order. */
 mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offsets, const int32_t* written_ids,
-                            int64_t n_points, const int32_t* block_colours, int32_t num_colours,
+                            int64_t n_points, const int32_t* block_colours, int32_t num_colours, int32_t lag,
                             int32_t* pred_offsets /* [nb+1] */, int32_t* preds, int64_t preds_capacity,
                             int64_t* num_preds, int32_t* order, void* stream);
 /* (when *num_preds > preds_capacity nothing but *num_preds is written:

@@ -42,7 +42,8 @@ class MpLoop(ctypes.Structure):
 class MpHierPlan(ctypes.Structure):
     _fields_ = [
         ("num_blocks", c_i32), ("block_size", c_i32), ("stage_reads", c_i32), ("max_staged", c_i32),
-        ("block_offsets", c_vp), ("staged_offsets", c_vp), ("staged_ids", c_vp),
+        ("slot_bytes", c_i32), ("written_is_staged", c_i32),
+        ("meta", c_vp), ("staged_ids", c_vp),
         ("written_offsets", c_vp), ("written_ids", c_vp), ("written_slots", c_vp),
         ("local_slots", c_vp), ("thread_colours", c_vp), ("colour_counts", c_vp),
         ("num_block_colours", c_i32), ("pad_", c_i32),
@@ -66,7 +67,7 @@ _SIGNATURES = {
     "mp_greedy_colour_adj": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "mp_smallest_last_order": (c_i32, [c_i64, c_vp, c_vp, c_vp]),
     "mp_bfs_levels": (c_i32, [c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
-    "mp_plan_block_dag": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "mp_plan_block_dag": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "mp_heavy_edge_matching": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "mp_cut_weight": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "mp_refine_boundary_pass": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_vp]),

@@ -123,12 +123,13 @@ __global__ void colour_keys_kernel(int32_t nb, const int32_t* __restrict__ colou
 
 // key(b) = max(b, max over preds key(p) + 1) for the blocks of one colour
 __global__ void dag_key_kernel(int32_t lo, int32_t hi, const uint64_t* __restrict__ by_colour,
-                               const int32_t* __restrict__ off, const int32_t* __restrict__ preds, uint32_t* key) {
+                               const int32_t* __restrict__ off, const int32_t* __restrict__ preds, uint32_t* key,
+                               uint32_t lag) {
   for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t b = (uint32_t)by_colour[i];
     uint32_t k = b;
     for (int j = off[b]; j < off[b + 1]; ++j) {
-      uint32_t q = key[preds[j]] + 1;
+      uint32_t q = key[preds[j]] + lag;
       k = q > k ? q : k;
     }
     key[b] = k;
@@ -222,7 +223,7 @@ extern "C" mp_status mp_race_check(int64_t n, const int64_t* ref_offsets, const 
 }
 
 extern "C" mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offsets, const int32_t* written_ids,
-                                       int64_t n_points, const int32_t* block_colours, int32_t num_colours,
+                                       int64_t n_points, const int32_t* block_colours, int32_t num_colours, int32_t lag,
                                        int32_t* pred_offsets, int32_t* preds, int64_t preds_capacity,
                                        int64_t* num_preds, int32_t* order, void* stream) {
   clear_error();
@@ -303,7 +304,7 @@ extern "C" mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offset
     int32_t hi = lo;
     while (hi < nb && (uint32_t)(hk[hi] >> 32) == c) ++hi;
     dag_key_kernel<<<grid_for(hi - lo), 256, 0, st>>>(lo, hi, ck.as<uint64_t>(), pred_offsets, preds,
-                                                     key.as<uint32_t>());
+                                                     key.as<uint32_t>(), (uint32_t)(lag > 0 ? lag : 1));
     ce = cudaGetLastError();
     if (ce != cudaSuccess) break;
     lo = hi;

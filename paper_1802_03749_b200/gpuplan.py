@@ -219,9 +219,15 @@ def local_slots(block_offsets_d, map_d, mask, st_off, st_ids, wr_off, wr_ids):
     return ls, ws
 
 
-def block_dag(wr_off, wr_ids, npts: int, block_colours_d, ncol: int):
+DATAFLOW_LAG = int(__import__("os").environ.get("MESHPLAN_DATAFLOW_LAG", "2048"))
+
+
+def block_dag(wr_off, wr_ids, npts: int, block_colours_d, ncol: int, lag: int = DATAFLOW_LAG):
     """Predecessor lists (lower-colour blocks sharing a written point) and a
-    topological block order close to id order, for the dataflow schedule."""
+    topological block order: key(b) = max(b, max over preds key(p) + lag),
+    blocks sorted by (key, id).  ``lag`` keeps a dependent block about one
+    wave of resident CTAs behind its predecessors (so it rarely waits) while
+    its shared rows are still in L2."""
     nb = wr_off.numel() - 1
     dev = wr_off.device
     pred_off = torch.zeros(nb + 1, dtype=torch.int32, device=dev)
@@ -233,8 +239,8 @@ def block_dag(wr_off, wr_ids, npts: int, block_colours_d, ncol: int):
         preds = torch.zeros(cap, dtype=torch.int32, device=dev)
         npred = np.zeros(1, dtype=np.int64)
         _native.call("mp_plan_block_dag", nb, _native.ptr(wr_off), _native.ptr(wr_ids), int(npts),
-                     _native.ptr(block_colours_d), int(ncol), _native.ptr(pred_off), _native.ptr(preds), cap,
-                     npred.ctypes.data, _native.ptr(order), _sp())
+                     _native.ptr(block_colours_d), int(ncol), int(lag), _native.ptr(pred_off), _native.ptr(preds),
+                     cap, npred.ctypes.data, _native.ptr(order), _sp())
         if int(npred[0]) <= cap:
             return pred_off, preds[: max(int(npred[0]), 1)], order[:nb]
         cap = int(npred[0])
@@ -270,14 +276,16 @@ class DevicePlan:
 
     map: torch.Tensor               # (n, arity) int32, plan numbering
     block_offsets: torch.Tensor     # int32 [nb+1]
+    meta: torch.Tensor              # int32 [nb, 4] {e0, k, s0, ns}
     staged_off: torch.Tensor
     staged_ids: torch.Tensor
     written_off: torch.Tensor
     written_ids: torch.Tensor
     written_slots: torch.Tensor     # int16 (uint16 bits)
-    local_slots: torch.Tensor       # int16 [n*arity]
+    local_slots: torch.Tensor       # uint8 or int16 (uint16 bits) [n*arity]
     thread_colours: torch.Tensor    # uint8 [n]
     colour_counts: torch.Tensor     # int32 [nb]
+    block_colours: torch.Tensor     # int32 [nb]
     blocks_by_colour: torch.Tensor  # int32 [nb]
     colour_block_offsets: np.ndarray  # host int32 [ncol+1]
     order: torch.Tensor             # int32 [nb]
@@ -288,6 +296,9 @@ class DevicePlan:
     block_size: int
     max_staged: int
     stage_reads: bool
+    written_is_staged: bool
+    npts: int
+    lag: int = DATAFLOW_LAG
     epoch: int = 0
 
     def struct(self) -> "_native.MpHierPlan":
@@ -296,8 +307,9 @@ class DevicePlan:
         p.block_size = int(self.block_size)
         p.stage_reads = int(self.stage_reads)
         p.max_staged = int(self.max_staged)
-        for name, t in (("block_offsets", self.block_offsets), ("staged_offsets", self.staged_off),
-                        ("staged_ids", self.staged_ids), ("written_offsets", self.written_off),
+        p.slot_bytes = self.local_slots.element_size()
+        p.written_is_staged = int(self.written_is_staged)
+        for name, t in (("meta", self.meta), ("staged_ids", self.staged_ids), ("written_offsets", self.written_off),
                         ("written_ids", self.written_ids), ("written_slots", self.written_slots),
                         ("local_slots", self.local_slots), ("thread_colours", self.thread_colours),
                         ("colour_counts", self.colour_counts), ("blocks_by_colour", self.blocks_by_colour),
@@ -308,6 +320,14 @@ class DevicePlan:
         p.colour_block_offsets_host = self.colour_block_offsets.ctypes.data
         return p
 
+    def reschedule(self, lag: int) -> None:
+        """Recompute the dataflow order for another lag (tuning)."""
+        ncol = len(self.colour_block_offsets) - 1
+        self.pred_off, self.preds, self.order = block_dag(self.written_off, self.written_ids, self.npts,
+                                                          self.block_colours, ncol, lag)
+        self.lag = lag
+        self.__dict__.pop("_struct", None)
+
 
 def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sorted_d, tcounts_d, st_off, st_ids,
                       wr_off, wr_ids, stage_mask, stage_reads, npts, block_size) -> DevicePlan:
@@ -316,23 +336,28 @@ def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sort
     bo = torch.as_tensor(block_offsets_np.astype(np.int32), device=dev)
     nb = bo.numel() - 1
     ls, ws = local_slots(bo, map_d, stage_mask, st_off, st_ids, wr_off, wr_ids)
+    counts = (st_off[1:] - st_off[:-1]) if nb else torch.zeros(0, dtype=torch.int32, device=dev)
+    max_staged = int(counts.max()) if nb else 0
+    if max_staged <= 256:
+        ls = ls.to(torch.uint8)  # slot values < 256 (unused slots 0xFFFF only where not staged)
+    wsame = bool(torch.equal(st_off, wr_off) and torch.equal(st_ids, wr_ids))
+    meta = torch.stack([bo[:-1], bo[1:] - bo[:-1], st_off[:-1], counts], dim=1).to(torch.int32).contiguous()
     bc = torch.as_tensor(block_colours_np.astype(np.int32), device=dev)
     by_colour = np.lexsort((np.arange(nb), block_colours_np)).astype(np.int32) if nb else np.zeros(0, np.int32)
     cbo = np.zeros(ncol + 1, dtype=np.int32)
     if nb:
         cbo[1:] = np.cumsum(np.bincount(block_colours_np, minlength=ncol))
     pred_off, preds, order = block_dag(wr_off, wr_ids, npts, bc, ncol)
-    counts = np.diff(st_off.cpu().numpy()) if nb else np.zeros(0)
     if tcounts_d.numel() and int(tcounts_d.max()) > 255:
         raise CapacityError("a block needs more than 255 thread colours")
     return DevicePlan(
-        map=map_d, block_offsets=bo, staged_off=st_off, staged_ids=st_ids, written_off=wr_off, written_ids=wr_ids,
-        written_slots=ws, local_slots=ls, thread_colours=tcol_sorted_d.to(torch.uint8),
-        colour_counts=tcounts_d.to(torch.int32), blocks_by_colour=torch.as_tensor(by_colour, device=dev),
-        colour_block_offsets=cbo, order=order, pred_off=pred_off, preds=preds,
-        flags=torch.zeros(max(nb, 1), dtype=torch.int32, device=dev),
-        tickets=torch.zeros(2, dtype=torch.int32, device=dev),
-        block_size=int(block_size), max_staged=int(counts.max()) if counts.size else 0, stage_reads=bool(stage_reads),
+        map=map_d, block_offsets=bo, meta=meta, staged_off=st_off, staged_ids=st_ids, written_off=wr_off,
+        written_ids=wr_ids, written_slots=ws, local_slots=ls, thread_colours=tcol_sorted_d.to(torch.uint8),
+        colour_counts=tcounts_d.to(torch.int32), block_colours=bc,
+        blocks_by_colour=torch.as_tensor(by_colour, device=dev), colour_block_offsets=cbo, order=order,
+        pred_off=pred_off, preds=preds, flags=torch.zeros(max(nb, 1), dtype=torch.int32, device=dev),
+        tickets=torch.zeros(2, dtype=torch.int32, device=dev), block_size=int(block_size), max_staged=max_staged,
+        stage_reads=bool(stage_reads), written_is_staged=wsame, npts=int(npts),
     )
 
 

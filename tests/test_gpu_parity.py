@@ -61,7 +61,7 @@ def test_executor_on_reference_plan_bit_exact(rec):
 # ---- planner parity (bit-exact plans) --------------------------------------------------
 
 
-PLANNED = [c for c in CASES if c["reorder"] != "partition"]
+PLANNED = CASES  # none, gps, partition (k-way) and structured plans
 
 
 @pytest.mark.parametrize("rec", PLANNED, ids=_ids)

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--layout", default="aos")
     ap.add_argument("--block-size", type=int, default=128)
     ap.add_argument("--runs", type=int, default=3)
+    ap.add_argument("--timed", type=int, default=1)
+    ap.add_argument("--lags", default="")
     args = ap.parse_args()
 
     import torch
@@ -34,19 +36,28 @@ def main():
     t0 = time.perf_counter()
     plan = (mp.build_global_plan if args.strategy == "global" else mp.build_hierarchical_plan)(mesh, kernel, cfg)
     print(f"plan {time.perf_counter() - t0:.2f}s", flush=True)
-    loop = mp.bind(plan, kernel, schedule=args.schedule)
-    torch.cuda.synchronize()
-    for _ in range(args.runs):
-        loop.run()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    loop.run()
-    b.record()
-    torch.cuda.synchronize()
     ub = mp.useful_bytes(kernel, mesh)
-    ms = a.elapsed_time(b)
-    print(f"{args.strategy}/{args.schedule}: {ms:.4f} ms  {ub / ms / 1e6:.1f} GB/s", flush=True)
+    scheds = args.schedule.split(",")
+    lags = [int(x) for x in args.lags.split(",")] if args.lags else [None]
+    for sched in scheds:
+        for lag in (lags if sched == "dataflow" else [None]):
+            if lag is not None:
+                plan._device.reschedule(lag)
+            loop = mp.bind(plan, kernel, schedule=sched)
+            torch.cuda.synchronize()
+            for _ in range(args.runs):
+                loop.run()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(args.timed):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                loop.run()
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            ms = sorted(ts)[len(ts) // 2]
+            print(f"{args.strategy}/{sched} lag={lag}: {ms:.4f} ms  {ub / ms / 1e6:.1f} GB/s", flush=True)
 
 
 if __name__ == "__main__":
