@@ -124,6 +124,15 @@ mp_status mp_exec_global(const mp_loop* loop, const int64_t* colour_offsets, int
 mp_status mp_exec_hier(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule, uint32_t epoch,
                        void* stream);
 
+/* Same semantics and results as mp_exec_hier, as a persistent
+ * warp-specialised kernel: one producer warp per CTA fills a 3-stage
+ * mbarrier ring with cp.async gathers (staged ids and rows, increment rows,
+ * slots, direct operands, colours) ahead of the consumer warps.  Needs
+ * written_is_staged and block_size <= 992.  MP_SCHED_DATAFLOW: the producer
+ * acquires the predecessors' flags before gathering increment rows. */
+mp_status mp_exec_hier_pipelined(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule, uint32_t epoch,
+                                 void* stream);
+
 /* execute_serial (simulator.py:215-230) on the device: per-element
  * increments to a temp array, then per point an ordered sum over its
  * (element, slot) references (inverse CSR, mesh.py:251-267), i.e. exactly the

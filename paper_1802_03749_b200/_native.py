@@ -58,7 +58,8 @@ _SIGNATURES = {
     "mp_device_sm_count": (c_i32, [c_i32]),
     "mp_exec_global": (c_i32, [ctypes.POINTER(MpLoop), c_vp, c_i32, c_i32, c_vp]),
     "mp_exec_hier": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_u32, c_vp]),
-    "mp_exec_serial": (c_i32, [ctypes.POINTER(MpLoop), c_vp, c_vp, c_vp, c_vp]),
+    "mp_exec_hier_pipelined": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_u32, c_vp]),
+    "mp_exec_serial":(c_i32, [ctypes.POINTER(MpLoop), c_vp, c_vp, c_vp, c_vp]),
     "mp_race_check": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "mp_plan_block_points": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_i32, c_u32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "mp_plan_local_slots": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_i32, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

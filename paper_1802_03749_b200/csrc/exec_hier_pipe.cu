@@ -1,0 +1,405 @@
+// X2, pipelined: persistent, warp-specialised hierarchical executor.
+//
+// Same block semantics as exec_hier.cu (stage -> compute -> thread-colour
+// loop in shared memory -> one write-back per block; bit-identical results),
+// restructured the Blackwell way so that no consumer warp ever waits on HBM:
+//
+//   * grid = resident CTAs (persistent); each CTA = 1 producer warp + one
+//     consumer thread per block element;
+//   * a ring of NSTAGE shared-memory stages guarded by mbarriers
+//     (full: 32 explicit + 32 cp.async.mbarrier arrivals; empty: 1 arrival);
+//   * the producer warp claims the next block (colour list, or a dataflow
+//     ticket), and fills a stage with cp.async (LDGSTS): the block's staged
+//     ids, its staged read rows and increment rows (gathered through the
+//     ascending deduplicated staged list), the element-local slot indices,
+//     direct operands and thread colours -- NSTAGE blocks ahead of the
+//     consumers;
+//   * consumers compute from shared memory, apply increments one thread
+//     colour at a time (named barrier among consumer warps only), write
+//     row + increment back once, and release the stage.
+//
+// Dataflow schedule: the producer checks the block's lower-colour
+// predecessors' flags (acquire) before gathering the increment rows, so the
+// rows it prefetches already contain every earlier writer's contribution;
+// consumers never wait.  Tickets are claimed in a topological order, so a
+// producer only ever waits on smaller tickets, which are either finished,
+// sitting in some stage (consumers never block), or being claimed by a
+// producer that waits on still smaller tickets: no deadlock.
+#include "mp_loop.cuh"
+
+namespace mp {
+namespace {
+
+constexpr int NSTAGE = 3;
+
+__device__ __forceinline__ unsigned saddr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cpasync(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
+          saddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int BYTES>
+__device__ __forceinline__ void cpa(void* dst, const void* src) {
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr(dst)), "l"(src) : "memory");
+  else if constexpr (BYTES == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr(dst)), "l"(src) : "memory");
+}
+
+constexpr int vbytes(int row_bytes) { return row_bytes % 16 == 0 ? 16 : (row_bytes % 8 == 0 ? 8 : 4); }
+constexpr int align16(int x) { return (x + 15) & ~15; }
+
+struct PipeView {
+  const int4* __restrict__ meta;
+  const int32_t* __restrict__ staged_ids;
+  const unsigned char* __restrict__ local_slots;
+  const uint8_t* __restrict__ tcol;
+  const int32_t* __restrict__ ncol;
+  const int32_t* __restrict__ list;  // colour: blocks of this colour; dataflow: ticket order
+  int32_t list_len;
+  const int32_t* __restrict__ pred_offsets;
+  const int32_t* __restrict__ preds;
+  uint32_t* flags;
+  uint32_t* tickets;
+  uint32_t epoch;
+  int32_t stage_reads;
+  int32_t max_staged;
+  int32_t max_block;
+};
+
+// Byte layout of one stage, computed identically on host and device.
+template <class Op, typename T, typename SlotT>
+struct StageLayout {
+  static constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC;
+  int hdr, ids, rows_q, rows_r, slots, dir, tc, bytes, dir_pitch, q_rows;
+  __host__ __device__ StageLayout(int max_staged, int max_block, bool stage_reads) {
+    const int qrows = RC == 0 ? 0 : (stage_reads ? max_staged : max_block * A);  // staged or per (elem, slot)
+    q_rows = qrows;
+    dir_pitch = max_block + 8;  // + alignment slack (copies start at a 16 B boundary)
+    hdr = 0;
+    ids = 64;
+    rows_q = align16(ids + max_staged * 4);
+    rows_r = align16(rows_q + qrows * RC * (int)sizeof(T));
+    slots = align16(rows_r + max_staged * IC * (int)sizeof(T));
+    dir = align16(slots + max_block * A * (int)sizeof(SlotT) + 16);
+    tc = align16(dir + DC * dir_pitch * (int)sizeof(T));
+    bytes = align16(tc + max_block + 16);
+  }
+};
+
+// header ints: 0 block (-1: stop), 1 e0, 2 k, 3 ns, 4 ncol, 5 slot byte delta, 6 dir elem delta, 7 tc delta
+
+template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT>
+__global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView H) {
+  constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const StageLayout<Op, T, SlotT> L(H.max_staged, H.max_block, H.stage_reads != 0);
+  const int nthreads = blockDim.x;
+  const int nc_threads = nthreads - 32;  // consumers: warps 1..
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + NSTAGE;
+  T* sh_inc = reinterpret_cast<T*>(smem + 128);
+  unsigned char* stage0 = smem + 128 + align16(H.max_staged * IC * (int)sizeof(T));
+  const bool stage_reads = RC > 0 && H.stage_reads;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 64);
+      mbar_init(&empty[s], 1);
+    }
+  }
+  for (int i = threadIdx.x; i < H.max_staged * IC; i += nthreads) sh_inc[i] = T(0);
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------- producer -------------------------------
+    int iter = 0;
+    for (int fill = 0;; ++fill) {
+      const int s = fill % NSTAGE;
+      unsigned char* st = stage0 + s * L.bytes;
+      int* hdr = reinterpret_cast<int*>(st);
+      mbar_wait(&empty[s], ((fill / NSTAGE) & 1) ^ 1);
+      int b = -1;
+      if (lane == 0) {
+        if constexpr (DATAFLOW) {
+          const uint32_t t = atomicAdd(&H.tickets[0], 1u);
+          b = t < (uint32_t)H.list_len ? __ldg(H.list + t) : -1;
+        } else {
+          const int i = blockIdx.x + iter * gridDim.x;
+          b = i < H.list_len ? __ldg(H.list + i) : -1;
+        }
+      }
+      ++iter;
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (b < 0) {
+        if (lane == 0) hdr[0] = -1;
+        mbar_arrive(&full[s]);
+        mbar_arrive_cpasync(&full[s]);
+        break;
+      }
+      const int4 md = __ldg(H.meta + b);
+      const int e0 = md.x, k = md.y, s0 = md.z, ns = md.w;
+      // element-local data: slots, direct planes, colours (aligned-down 4 B copies)
+      const int64_t sl_lo = ((int64_t)e0 * A * (int)sizeof(SlotT)) & ~int64_t(3);
+      const int sl_delta = (int)((int64_t)e0 * A * (int)sizeof(SlotT) - sl_lo);
+      const int sl_words = (sl_delta + k * A * (int)sizeof(SlotT) + 3) >> 2;
+      for (int i = lane; i < sl_words; i += 32)
+        cpa<4>(st + L.slots + 4 * i, H.local_slots + sl_lo + 4 * i);
+      const int64_t tc_lo = (int64_t)e0 & ~int64_t(3);
+      const int tc_delta = (int)(e0 - tc_lo);
+      const int tc_words = (tc_delta + k + 3) >> 2;
+      for (int i = lane; i < tc_words; i += 32) cpa<4>(st + L.tc + 4 * i, H.tcol + tc_lo + 4 * i);
+      constexpr int DW = (int)sizeof(T) >= 4 ? 1 : 4 / (int)sizeof(T);
+      const int64_t d_lo = (int64_t)e0 & ~int64_t(DW - 1);
+      const int d_delta = (int)(e0 - d_lo);
+      for (int c = 0; c < DC; ++c) {
+        const T* src = v.dir + (int64_t)c * v.n + d_lo;
+        T* dst = reinterpret_cast<T*>(st + L.dir) + c * L.dir_pitch;
+        const int nel = d_delta + k;
+        if constexpr (sizeof(T) >= 4) {
+          for (int i = lane; i < nel; i += 32) cpa<(int)sizeof(T)>(dst + i, src + i);
+        }
+      }
+      if (lane == 0) {
+        hdr[0] = b;
+        hdr[1] = e0;
+        hdr[2] = k;
+        hdr[3] = ns;
+        hdr[4] = __ldg(H.ncol + b);
+        hdr[5] = sl_delta;
+        hdr[6] = d_delta;
+        hdr[7] = tc_delta;
+      }
+      // staged ids -> registers + stage; gathers of the staged rows
+      int* ids = reinterpret_cast<int*>(st + L.ids);
+      T* rq = reinterpret_cast<T*>(st + L.rows_q);
+      T* rr = reinterpret_cast<T*>(st + L.rows_r);
+      if constexpr (DATAFLOW) {  // predecessors must have written back before we read rows
+        const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
+        for (int i = lane; i < nq; i += 32) {
+          const uint32_t* f = H.flags + __ldg(H.preds + q0 + i);
+          while (ld_acquire_gpu(f) != H.epoch) __nanosleep(20);
+        }
+        __syncwarp();
+      }
+      for (int j = lane; j < ns; j += 32) {
+        const int p = __ldg(H.staged_ids + s0 + j);
+        ids[j] = p;
+        if constexpr (LAYOUT == MP_AOS) {
+          constexpr int VR = vbytes(IC * (int)sizeof(T));
+#pragma unroll
+          for (int ch = 0; ch < IC * (int)sizeof(T) / VR; ++ch)
+            cpa<VR>(reinterpret_cast<unsigned char*>(rr + j * IC) + ch * VR,
+                    reinterpret_cast<const unsigned char*>(v.inc + (int64_t)p * IC) + ch * VR);
+          if (RC > 0 && H.stage_reads) {
+            constexpr int RCB = RC > 0 ? RC : 1;
+            constexpr int VQ = vbytes(RCB * (int)sizeof(T));
+            if ((v.ind_comps * (int)sizeof(T)) % VQ == 0) {
+#pragma unroll
+              for (int ch = 0; ch < RCB * (int)sizeof(T) / VQ; ++ch)
+                cpa<VQ>(reinterpret_cast<unsigned char*>(rq + j * RCB) + ch * VQ,
+                        reinterpret_cast<const unsigned char*>(v.ind + (int64_t)p * v.ind_comps) + ch * VQ);
+            } else {
+#pragma unroll
+              for (int c = 0; c < RCB; ++c) cpa<(int)sizeof(T)>(rq + j * RCB + c, v.ind + (int64_t)p * v.ind_comps + c);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < IC; ++c) cpa<(int)sizeof(T)>(rr + j * IC + c, v.inc + (int64_t)c * v.npts + p);
+          if (RC > 0 && H.stage_reads) {
+#pragma unroll
+            for (int c = 0; c < RC; ++c) cpa<(int)sizeof(T)>(rq + j * RCN + c, v.ind + (int64_t)c * v.npts + p);
+          }
+        }
+      }
+      if (RC > 0 && !H.stage_reads) {  // increment-only staging: read rows per (element, slot) via the mapping
+        for (int i = lane; i < k * A; i += 32) {
+          const int t = i / A, sl = i - t * A;
+          const int p = map_at(v, (int64_t)e0 + t, sl);
+#pragma unroll
+          for (int c = 0; c < RCN; ++c) cpa<(int)sizeof(T)>(rq + i * RCN + c, v.ind + ind_index<LAYOUT>(p, c, v.ind_comps, v.npts));
+        }
+      }
+      mbar_arrive(&full[s]);          // releases the header / ids stores
+      mbar_arrive_cpasync(&full[s]);  // fires when this lane's copies land
+    }
+  } else {
+    // ------------------------------- consumers ------------------------------
+    const int t = threadIdx.x - 32;
+    for (int use = 0;; ++use) {
+      const int s = use % NSTAGE;
+      unsigned char* st = stage0 + s * L.bytes;
+      const int* hdr = reinterpret_cast<const int*>(st);
+      mbar_wait(&full[s], (use / NSTAGE) & 1);
+      const int b = hdr[0];
+      if (b < 0) break;
+      const int k = hdr[2], ns = hdr[3], nc = hdr[4];
+      const int* ids = reinterpret_cast<const int*>(st + L.ids);
+      const T* rq = reinterpret_cast<const T*>(st + L.rows_q);
+      const T* rr = reinterpret_cast<const T*>(st + L.rows_r);
+      T o[A][IC];
+      int ls[A];
+      int my_tc = -1;
+      if (t < k) {
+        const SlotT* sl = reinterpret_cast<const SlotT*>(st + L.slots + hdr[5]) + t * A;
+#pragma unroll
+        for (int q = 0; q < A; ++q) ls[q] = sl[q];
+        T d[DC];
+        const T* dir = reinterpret_cast<const T*>(st + L.dir) + hdr[6] + t;
+#pragma unroll
+        for (int c = 0; c < DC; ++c) d[c] = dir[c * L.dir_pitch];
+        T r[A][RCN];
+        if (RC > 0) {
+          if (stage_reads) {
+#pragma unroll
+            for (int q = 0; q < A; ++q)
+#pragma unroll
+              for (int c = 0; c < RC; ++c) r[q][c] = rq[ls[q] * RCN + c];
+          } else {
+#pragma unroll
+            for (int q = 0; q < A; ++q)
+#pragma unroll
+              for (int c = 0; c < RC; ++c) r[q][c] = rq[(t * A + q) * RCN + c];
+          }
+        }
+        compute<Op, T>(v, r, d, o);
+        my_tc = (st + L.tc)[hdr[7] + t];
+      }
+      for (int c = 0; c < nc; ++c) {
+        if (my_tc == c) {
+#pragma unroll
+          for (int q = 0; q < A; ++q)
+#pragma unroll
+            for (int cc = 0; cc < IC; ++cc) sh_inc[ls[q] * IC + cc] += o[q][cc];
+        }
+        named_sync(1, nc_threads);
+      }
+      if (nc == 0) named_sync(1, nc_threads);
+      // write back rows + increments, re-zero the increment region
+      if constexpr (LAYOUT == MP_AOS) {
+        for (int i = t; i < ns * IC; i += nc_threads) {
+          const int j = i / IC, c = i - j * IC;
+          v.inc[(int64_t)ids[j] * IC + c] = rr[i] + sh_inc[i];
+          sh_inc[i] = T(0);
+        }
+      } else {
+        for (int i = t; i < ns * IC; i += nc_threads) {
+          const int c = i / ns, j = i - c * ns;
+          v.inc[(int64_t)c * v.npts + ids[j]] = rr[j * IC + c] + sh_inc[j * IC + c];
+        }
+        named_sync(1, nc_threads);
+        for (int i = t; i < ns * IC; i += nc_threads) sh_inc[i] = T(0);
+      }
+      named_sync(1, nc_threads);
+      if (t == 0) {
+        if constexpr (DATAFLOW) {
+          __threadfence();
+          st_release_gpu(H.flags + b, H.epoch);
+        }
+        mbar_arrive(&empty[s]);
+      }
+    }
+  }
+  if constexpr (DATAFLOW) {
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&H.tickets[1], 1u) == gridDim.x - 1) {
+      H.tickets[0] = 0u;  // last CTA out re-arms the counters
+      H.tickets[1] = 0u;
+    }
+  }
+}
+
+template <class Op, typename T, int LAYOUT, typename SlotT>
+mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
+  const StageLayout<Op, T, SlotT> L(P.max_staged, P.block_size, P.stage_reads != 0);
+  const size_t smem = 128 + ((P.max_staged * Op::IC * sizeof(T) + 15) & ~size_t(15)) + (size_t)NSTAGE * L.bytes;
+  if (smem > 227 * 1024)
+    MP_FAIL(MP_ERR_CAPACITY, "pipelined stages need %zu shared bytes, over the 232448-byte limit", smem);
+  const int consumers = ((P.block_size + 31) / 32) * 32;
+  const int threads = consumers + 32;
+  auto kern = dataflow ? hier_pipe_kernel<Op, T, LAYOUT, true, SlotT> : hier_pipe_kernel<Op, T, LAYOUT, false, SlotT>;
+  MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0, dev = 0, sms = 0;
+  MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  MP_CUDA_TRY(cudaGetDevice(&dev));
+  MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (per_sm < 1) MP_FAIL(MP_ERR_CAPACITY, "pipelined executor does not fit on an SM (%zu shared bytes)", smem);
+  const int resident = per_sm * sms;
+  if (dataflow) {
+    H.list = P.order;
+    H.list_len = P.num_blocks;
+    const int grid = P.num_blocks < resident ? P.num_blocks : resident;
+    kern<<<grid, threads, smem, st>>>(v, H);
+    MP_CHECK_LAUNCH();
+    return MP_OK;
+  }
+  for (int c = 0; c < P.num_block_colours; ++c) {
+    const int lo = P.colour_block_offsets_host[c], hi = P.colour_block_offsets_host[c + 1];
+    if (hi <= lo) continue;
+    H.list = P.blocks_by_colour + lo;
+    H.list_len = hi - lo;
+    const int grid = (hi - lo) < resident ? (hi - lo) : resident;
+    kern<<<grid, threads, smem, st>>>(v, H);
+    MP_CHECK_LAUNCH();
+  }
+  return MP_OK;
+}
+
+template <class Op, typename T>
+mp_status launch_pipe_op(const mp_loop& Lp, const mp_hier_plan& P, bool dataflow, uint32_t epoch, cudaStream_t st) {
+  if constexpr (!op_supported<Op, T>()) {
+    MP_FAIL(MP_ERR_KERNEL, "heavy face flux needs float data");
+  } else {
+    mp_status s = check_loop_shape(Lp, Op::ARITY, Op::RC, Op::DC, Op::IC);
+    if (s) return s;
+    if (P.num_blocks == 0) return MP_OK;
+    if (!P.written_is_staged) MP_FAIL(MP_ERR_KERNEL, "pipelined executor needs written lists equal to staged lists");
+    if (P.block_size > 992) MP_FAIL(MP_ERR_CAPACITY, "block size %d exceeds 992 (+1 producer warp)", P.block_size);
+    PipeView H{reinterpret_cast<const int4*>(P.meta), P.staged_ids,
+               static_cast<const unsigned char*>(P.local_slots), P.thread_colours, P.colour_counts,
+               nullptr, 0, P.pred_offsets, P.preds, P.flags, P.tickets, epoch, P.stage_reads, P.max_staged,
+               P.block_size};
+    LoopView<T> v = make_view<T>(Lp);
+    const bool u8 = P.slot_bytes == 1;
+    if (Lp.ind_layout == MP_AOS)
+      return u8 ? launch_pipe<Op, T, MP_AOS, uint8_t>(v, H, P, dataflow, st)
+                : launch_pipe<Op, T, MP_AOS, uint16_t>(v, H, P, dataflow, st);
+    return u8 ? launch_pipe<Op, T, MP_SOA, uint8_t>(v, H, P, dataflow, st)
+              : launch_pipe<Op, T, MP_SOA, uint16_t>(v, H, P, dataflow, st);
+  }
+}
+
+}  // namespace
+}  // namespace mp
+
+extern "C" mp_status mp_exec_hier_pipelined(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule,
+                                            uint32_t epoch, void* stream) {
+  mp::clear_error();
+  if (!loop || !plan) MP_FAIL(MP_ERR_KERNEL, "null argument");
+  const bool df = schedule == MP_SCHED_DATAFLOW;
+  if (df && epoch == 0) MP_FAIL(MP_ERR_KERNEL, "dataflow epochs start at 1");
+  cudaStream_t st = mp::as_stream(stream);
+  const mp_loop& L = *loop;
+  const mp_hier_plan& P = *plan;
+  return MP_DISPATCH_OP(L.op, [&]() {
+    return MP_DISPATCH_DTYPE(L.dtype, [&]() { return mp::launch_pipe_op<Op, scalar_t>(L, P, df, epoch, st); });
+  });
+}

@@ -24,7 +24,13 @@ from .kernelspec import KernelSpec
 from .mesh import DataArray, Mesh
 from .plan import GlobalPlan, HierarchicalPlan, MAPPING_ENTRY_BYTES, reuse_factor
 
-SCHEDULES = {"colour": _native.MP_SCHED_COLOUR, "dataflow": _native.MP_SCHED_DATAFLOW}
+#: schedule name -> (native schedule, pipelined persistent kernel?)
+SCHEDULES = {
+    "colour": (_native.MP_SCHED_COLOUR, False),
+    "dataflow": (_native.MP_SCHED_DATAFLOW, False),
+    "pipelined": (_native.MP_SCHED_COLOUR, True),
+    "pipelined-dataflow": (_native.MP_SCHED_DATAFLOW, True),
+}
 TORCH_DTYPES = {"f64": torch.float64, "f32": torch.float32, "i64": torch.int64, "i32": torch.int32}
 
 
@@ -153,6 +159,7 @@ class DeviceLoop:
     tensors: dict
     loop: _native.MpLoop
     schedule: int = _native.MP_SCHED_DATAFLOW
+    pipelined: bool = False
     launches: int = 0
     _keep: list = field(default_factory=list)
 
@@ -167,7 +174,8 @@ class DeviceLoop:
         else:
             if self.schedule == _native.MP_SCHED_DATAFLOW:
                 dp.epoch = dp.epoch % 0xFFFFFFFF + 1  # flags hold the last epoch; never 0
-            _native.call("mp_exec_hier", self.loop, dp.struct_cached(), self.schedule, max(dp.epoch, 1), sp)
+            fn = "mp_exec_hier_pipelined" if self.pipelined else "mp_exec_hier"
+            _native.call(fn, self.loop, dp.struct_cached(), self.schedule, max(dp.epoch, 1), sp)
 
     def run_host(self, inputs: dict, out, stream=None) -> None:
         """One end-to-end step with host buffers: H2D of the given arrays
@@ -232,7 +240,10 @@ def bind(plan, kernel: KernelSpec, tensors: dict | None = None, schedule: str = 
     L.dir_comps = mesh.data[dr.array].components
     L.inc = t[inc.array].data_ptr()
     L.inc_comps = inc_arr.components
-    return DeviceLoop(plan, kernel, t, L, SCHEDULES[schedule])
+    if schedule not in SCHEDULES:
+        raise KernelSpecError(f"unknown schedule {schedule!r}; expected one of {sorted(SCHEDULES)}")
+    sched, pipelined = SCHEDULES[schedule]
+    return DeviceLoop(plan, kernel, t, L, sched, pipelined)
 
 
 # ------------------------------------------------------------------------------
@@ -384,7 +395,8 @@ def _report(plan, kernel, loop: DeviceLoop, ms: float | None) -> MetricsReport:
         "hier", n, loop.launches_per_run(), plan.block_colours.num_colours, ub, tb, ops, occ, bps,
         reuse_factor(plan), int(plan.thread_colour_counts.max()) if nb else 0,
         float(plan.thread_colour_counts.mean()) if nb else 0.0, int(sync.sum()) if nb else 0, sync, smax, nb,
-        "dataflow" if loop.schedule == _native.MP_SCHED_DATAFLOW else "colour", ms, gbps,
+        ("pipelined-" if loop.pipelined else "") + ("dataflow" if loop.schedule == _native.MP_SCHED_DATAFLOW
+                                                    else "colour"), ms, gbps,
     )
 
 

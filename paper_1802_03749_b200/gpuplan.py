@@ -340,6 +340,9 @@ def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sort
     max_staged = int(counts.max()) if nb else 0
     if max_staged <= 256:
         ls = ls.to(torch.uint8)  # slot values < 256 (unused slots 0xFFFF only where not staged)
+    # 16 bytes of tail padding: the pipelined producer copies 4-byte aligned windows
+    ls = torch.cat([ls, torch.zeros(16 // ls.element_size(), dtype=ls.dtype, device=dev)])
+    tcol_sorted_d = torch.cat([tcol_sorted_d.to(torch.uint8), torch.zeros(16, dtype=torch.uint8, device=dev)])
     wsame = bool(torch.equal(st_off, wr_off) and torch.equal(st_ids, wr_ids))
     meta = torch.stack([bo[:-1], bo[1:] - bo[:-1], st_off[:-1], counts], dim=1).to(torch.int32).contiguous()
     bc = torch.as_tensor(block_colours_np.astype(np.int32), device=dev)

@@ -18,7 +18,7 @@ from helpers import config_of, reference_plan
 pytestmark = pytest.mark.gpu
 
 CASES = golden_cases()
-SCHEDULES = ("dataflow", "colour")
+SCHEDULES = ("dataflow", "colour", "pipelined", "pipelined-dataflow")
 
 
 def _ids(c):
@@ -226,10 +226,10 @@ def test_dataflow_repeated_runs_accumulate_exactly():
     mesh = mp.generate_mesh("quad2d", (128, 100), dtype="f64")
     kernel = mp.kernel_for_mesh("flux", mesh)
     plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps"))
-    loop_d = mp.bind(plan, kernel, schedule="dataflow")
-    loop_c = mp.bind(plan, kernel, schedule="colour")
+    loops = [mp.bind(plan, kernel, schedule=s) for s in SCHEDULES]
     for _ in range(7):
-        loop_d.run()
-        loop_c.run()
+        for lp in loops:
+            lp.run()
     torch.cuda.synchronize()
-    assert torch.equal(loop_d.tensors["res"], loop_c.tensors["res"])
+    for lp in loops[1:]:
+        assert torch.equal(loops[0].tensors["res"], lp.tensors["res"])
