@@ -130,32 +130,62 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
 
   if (warp == 0) {
     // ------------------------------- producer -------------------------------
-    int iter = 0;
+    // A 4-deep software pipeline hides the dependent chain claim -> block id ->
+    // descriptor -> staged ids: at fill f the warp claims block f+4, resolves
+    // the id of f+3, loads the descriptor of f+2 and prefetches (cp.async) the
+    // staged ids of f+1 into a 2-slot ring, then gathers block f's rows with
+    // ids already in shared memory.  Claims happen in fill order, which is the
+    // order the consumers drain the stages (required by the dataflow proof).
+    int* ring = reinterpret_cast<int*>(stage0 + NSTAGE * L.bytes);  // [2][max_staged] ids
+    int* mring = ring + 2 * H.max_staged;                          // [2][max_block*A] map rows
+    const bool map_rows = RC > 0 && !H.stage_reads;
+    auto claim = [&](int f) -> int {
+      if constexpr (DATAFLOW) return lane == 0 ? (int)atomicAdd(&H.tickets[0], 1u) : 0;
+      else return blockIdx.x + f * gridDim.x;
+    };
+    auto resolve = [&](int raw) -> int {
+      if constexpr (DATAFLOW) raw = __shfl_sync(0xffffffffu, raw, 0);
+      return (raw >= 0 && raw < H.list_len) ? __ldg(H.list + raw) : -1;
+    };
+    auto prefetch_ids = [&](int f, int bb, int4 m) {
+      if (bb < 0) return;
+      int* dst = ring + (f & 1) * H.max_staged;
+      for (int j = lane; j < m.w; j += 32) cpa<4>(dst + j, H.staged_ids + m.z + j);
+      if (map_rows) {
+        int* md = mring + (f & 1) * H.max_block * A;
+        for (int j = lane; j < m.y * A; j += 32) cpa<4>(md + j, v.map + (int64_t)m.x * A + j);
+      }
+    };
+    int raw1 = claim(0), raw2 = claim(1), raw3 = claim(2), raw4 = claim(3);
+    int b0 = resolve(raw1), b1 = resolve(raw2), b2 = resolve(raw3);
+    int4 md0 = b0 >= 0 ? __ldg(H.meta + b0) : make_int4(0, 0, 0, 0);
+    int4 md1 = b1 >= 0 ? __ldg(H.meta + b1) : make_int4(0, 0, 0, 0);
+    int nc0 = b0 >= 0 ? __ldg(H.ncol + b0) : 0;
+    int nc1 = b1 >= 0 ? __ldg(H.ncol + b1) : 0;
+    prefetch_ids(0, b0, md0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");  // empty "rows" group keeps the wait depth uniform
     for (int fill = 0;; ++fill) {
       const int s = fill % NSTAGE;
       unsigned char* st = stage0 + s * L.bytes;
       int* hdr = reinterpret_cast<int*>(st);
+      const int b = b0;
+      const int4 md = md0;
+      // advance the pipeline (results are consumed one fill later)
+      prefetch_ids(fill + 1, b1, md1);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      const int4 md2 = b2 >= 0 ? __ldg(H.meta + b2) : make_int4(0, 0, 0, 0);
+      const int nc2 = b2 >= 0 ? __ldg(H.ncol + b2) : 0;
+      const int b3 = resolve(raw4);
+      const int raw5 = claim(fill + 4);
       mbar_wait(&empty[s], ((fill / NSTAGE) & 1) ^ 1);
-      int b = -1;
-      if (lane == 0) {
-        if constexpr (DATAFLOW) {
-          const uint32_t t = atomicAdd(&H.tickets[0], 1u);
-          b = t < (uint32_t)H.list_len ? __ldg(H.list + t) : -1;
-        } else {
-          const int i = blockIdx.x + iter * gridDim.x;
-          b = i < H.list_len ? __ldg(H.list + i) : -1;
-        }
-      }
-      ++iter;
-      b = __shfl_sync(0xffffffffu, b, 0);
       if (b < 0) {
         if (lane == 0) hdr[0] = -1;
         mbar_arrive(&full[s]);
         mbar_arrive_cpasync(&full[s]);
         break;
       }
-      const int4 md = __ldg(H.meta + b);
-      const int e0 = md.x, k = md.y, s0 = md.z, ns = md.w;
+      const int e0 = md.x, k = md.y, ns = md.w;
       // element-local data: slots, direct planes, colours (aligned-down 4 B copies)
       const int64_t sl_lo = ((int64_t)e0 * A * (int)sizeof(SlotT)) & ~int64_t(3);
       const int sl_delta = (int)((int64_t)e0 * A * (int)sizeof(SlotT) - sl_lo);
@@ -182,12 +212,16 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
         hdr[1] = e0;
         hdr[2] = k;
         hdr[3] = ns;
-        hdr[4] = __ldg(H.ncol + b);
+        hdr[4] = nc0;
         hdr[5] = sl_delta;
         hdr[6] = d_delta;
         hdr[7] = tc_delta;
       }
-      // staged ids -> registers + stage; gathers of the staged rows
+      // staged ids (prefetched a fill ago) -> stage; gathers of the staged rows
+      asm volatile("cp.async.wait_group 2;" ::: "memory");  // this block's ids have landed
+      __syncwarp();
+      const int* rids = ring + (fill & 1) * H.max_staged;
+      const int* rmap = mring + (fill & 1) * H.max_block * A;
       int* ids = reinterpret_cast<int*>(st + L.ids);
       T* rq = reinterpret_cast<T*>(st + L.rows_q);
       T* rr = reinterpret_cast<T*>(st + L.rows_r);
@@ -200,7 +234,7 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
         __syncwarp();
       }
       for (int j = lane; j < ns; j += 32) {
-        const int p = __ldg(H.staged_ids + s0 + j);
+        const int p = rids[j];
         ids[j] = p;
         if constexpr (LAYOUT == MP_AOS) {
           constexpr int VR = vbytes(IC * (int)sizeof(T));
@@ -230,16 +264,25 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
           }
         }
       }
-      if (RC > 0 && !H.stage_reads) {  // increment-only staging: read rows per (element, slot) via the mapping
+      if (map_rows) {  // increment-only staging: read rows per (element, slot) via the mapping
         for (int i = lane; i < k * A; i += 32) {
-          const int t = i / A, sl = i - t * A;
-          const int p = map_at(v, (int64_t)e0 + t, sl);
+          const int p = rmap[i];
 #pragma unroll
           for (int c = 0; c < RCN; ++c) cpa<(int)sizeof(T)>(rq + i * RCN + c, v.ind + ind_index<LAYOUT>(p, c, v.ind_comps, v.npts));
         }
       }
       mbar_arrive(&full[s]);          // releases the header / ids stores
       mbar_arrive_cpasync(&full[s]);  // fires when this lane's copies land
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      // rotate the pipeline registers
+      b0 = b1;
+      b1 = b2;
+      b2 = b3;
+      md0 = md1;
+      md1 = md2;
+      nc0 = nc1;
+      nc1 = nc2;
+      raw4 = raw5;
     }
   } else {
     // ------------------------------- consumers ------------------------------
@@ -330,7 +373,9 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
 template <class Op, typename T, int LAYOUT, typename SlotT>
 mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
   const StageLayout<Op, T, SlotT> L(P.max_staged, P.block_size, P.stage_reads != 0);
-  const size_t smem = 128 + ((P.max_staged * Op::IC * sizeof(T) + 15) & ~size_t(15)) + (size_t)NSTAGE * L.bytes;
+  const size_t ring = (size_t)2 * P.max_staged * 4 + (size_t)2 * P.block_size * Op::ARITY * 4;
+  const size_t smem =
+      128 + ((P.max_staged * Op::IC * sizeof(T) + 15) & ~size_t(15)) + (size_t)NSTAGE * L.bytes + ring;
   if (smem > 227 * 1024)
     MP_FAIL(MP_ERR_CAPACITY, "pipelined stages need %zu shared bytes, over the 232448-byte limit", smem);
   const int consumers = ((P.block_size + 31) / 32) * 32;
