@@ -225,13 +225,17 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
       int* ids = reinterpret_cast<int*>(st + L.ids);
       T* rq = reinterpret_cast<T*>(st + L.rows_q);
       T* rr = reinterpret_cast<T*>(st + L.rows_r);
-      if constexpr (DATAFLOW) {  // predecessors must have written back before we read rows
+      // dataflow: prefetch the increment rows only if every lower-colour
+      // predecessor has already written back (one non-blocking acquire pass);
+      // otherwise the block is "late" and its consumers wait and read the rows
+      // at write-back time -- the producer never stalls the ring.
+      bool inc_rows = true;
+      if constexpr (DATAFLOW) {
         const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
-        for (int i = lane; i < nq; i += 32) {
-          const uint32_t* f = H.flags + __ldg(H.preds + q0 + i);
-          while (ld_acquire_gpu(f) != H.epoch) __nanosleep(20);
-        }
-        __syncwarp();
+        bool done = true;
+        for (int i = lane; i < nq; i += 32) done &= ld_acquire_gpu(H.flags + __ldg(H.preds + q0 + i)) == H.epoch;
+        inc_rows = __all_sync(0xffffffffu, done);
+        if (lane == 0) hdr[8] = inc_rows ? 0 : 1;
       }
       for (int j = lane; j < ns; j += 32) {
         const int p = rids[j];
@@ -240,8 +244,9 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
           constexpr int VR = vbytes(IC * (int)sizeof(T));
 #pragma unroll
           for (int ch = 0; ch < IC * (int)sizeof(T) / VR; ++ch)
-            cpa<VR>(reinterpret_cast<unsigned char*>(rr + j * IC) + ch * VR,
-                    reinterpret_cast<const unsigned char*>(v.inc + (int64_t)p * IC) + ch * VR);
+            if (inc_rows)
+              cpa<VR>(reinterpret_cast<unsigned char*>(rr + j * IC) + ch * VR,
+                      reinterpret_cast<const unsigned char*>(v.inc + (int64_t)p * IC) + ch * VR);
           if (RC > 0 && H.stage_reads) {
             constexpr int RCB = RC > 0 ? RC : 1;
             constexpr int VQ = vbytes(RCB * (int)sizeof(T));
@@ -257,7 +262,8 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < IC; ++c) cpa<(int)sizeof(T)>(rr + j * IC + c, v.inc + (int64_t)c * v.npts + p);
+          for (int c = 0; c < IC; ++c)
+            if (inc_rows) cpa<(int)sizeof(T)>(rr + j * IC + c, v.inc + (int64_t)c * v.npts + p);
           if (RC > 0 && H.stage_reads) {
 #pragma unroll
             for (int c = 0; c < RC; ++c) cpa<(int)sizeof(T)>(rq + j * RCN + c, v.ind + (int64_t)c * v.npts + p);
@@ -337,16 +343,30 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
       }
       if (nc == 0) named_sync(1, nc_threads);
       // write back rows + increments, re-zero the increment region
+      bool late = false;
+      if constexpr (DATAFLOW) {
+        late = hdr[8] != 0;
+        if (late) {  // the producer found a predecessor still running: wait, then read rows from L2
+          const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
+          for (int i = t; i < nq; i += nc_threads) {
+            const uint32_t* f = H.flags + __ldg(H.preds + q0 + i);
+            while (ld_acquire_gpu(f) != H.epoch) __nanosleep(32);
+          }
+          named_sync(1, nc_threads);
+        }
+      }
       if constexpr (LAYOUT == MP_AOS) {
         for (int i = t; i < ns * IC; i += nc_threads) {
           const int j = i / IC, c = i - j * IC;
-          v.inc[(int64_t)ids[j] * IC + c] = rr[i] + sh_inc[i];
+          T* a = v.inc + (int64_t)ids[j] * IC + c;
+          *a = (late ? ld_cg(a) : rr[i]) + sh_inc[i];
           sh_inc[i] = T(0);
         }
       } else {
         for (int i = t; i < ns * IC; i += nc_threads) {
           const int c = i / ns, j = i - c * ns;
-          v.inc[(int64_t)c * v.npts + ids[j]] = rr[j * IC + c] + sh_inc[j * IC + c];
+          T* a = v.inc + (int64_t)c * v.npts + ids[j];
+          *a = (late ? ld_cg(a) : rr[j * IC + c]) + sh_inc[j * IC + c];
         }
         named_sync(1, nc_threads);
         for (int i = t; i < ns * IC; i += nc_threads) sh_inc[i] = T(0);

@@ -40,7 +40,7 @@ def main():
     scheds = args.schedule.split(",")
     lags = [int(x) for x in args.lags.split(",")] if args.lags else [None]
     for sched in scheds:
-        for lag in (lags if sched == "dataflow" else [None]):
+        for lag in (lags if "dataflow" in sched else [None]):
             if lag is not None:
                 plan._device.reschedule(lag)
             loop = mp.bind(plan, kernel, schedule=sched)
