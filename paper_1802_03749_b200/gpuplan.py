@@ -219,7 +219,7 @@ def local_slots(block_offsets_d, map_d, mask, st_off, st_ids, wr_off, wr_ids):
     return ls, ws
 
 
-DATAFLOW_LAG = int(__import__("os").environ.get("MESHPLAN_DATAFLOW_LAG", "2048"))
+DATAFLOW_LAG = int(__import__("os").environ.get("MESHPLAN_DATAFLOW_LAG", "4096"))
 
 
 def block_dag(wr_off, wr_ids, npts: int, block_colours_d, ncol: int, lag: int = DATAFLOW_LAG):
