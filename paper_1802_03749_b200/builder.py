@@ -58,7 +58,7 @@ def _reorder(mesh, kernel, config, m: Mapping, map_d: torch.Tensor, fwd: dict):
     iter_set = kernel.iter_set_name(mesh)
     npts = m.to_set.size
     mode = config.reorder.split(":", 1)[0]
-    if mode in ("gps", "partition") and not kernel.indirect_args:
+    if mode in ("gps", "partition", "cluster") and not kernel.indirect_args:
         mode = "none"
     sizes, meta = None, {}
     if mode == "gps":
@@ -76,6 +76,21 @@ def _reorder(mesh, kernel, config, m: Mapping, map_d: torch.Tensor, fwd: dict):
         _compose(fwd, iter_set, _fwd_from_order(res.order))
         sizes = res.block_sizes
         meta = res.meta
+    elif mode == "cluster":  # extension: parallel GPU clustering blocks (see cluster.py)
+        from . import cluster, kway
+
+        pf_gps = gpuplan.gps_forward(map_d, npts)
+        gorder = gpuplan.lex_order(map_d, pf_gps, npts)
+        rank = torch.empty_like(gorder)
+        rank[gorder] = torch.arange(gorder.numel(), device=gorder.device)
+        order, _, sizes, meta = cluster.cluster_order(map_d, npts, config.block_size, rank)
+        assign = torch.empty_like(order)
+        assign[order] = torch.repeat_interleave(
+            torch.arange(len(sizes), device=order.device), torch.as_tensor(sizes, device=order.device))
+        pf = kway.writer_set_forward(map_d, npts, assign)
+        map_d = pf[map_d[order].long()].to(torch.int32)
+        _compose(fwd, m.to_set.name, pf)
+        _compose(fwd, iter_set, _fwd_from_order(order))
     elif mode == "structured":
         shape = config.structured_shape()
         family, dims = mesh.meta.get("family", ""), mesh.meta.get("dims", "")
@@ -173,8 +188,26 @@ def build_global(mesh: Mesh, kernel, config, hw) -> GlobalPlan:
     return plan
 
 
+class PhaseTimer:
+    """Wall time of planner phases (device synchronised at each mark)."""
+
+    def __init__(self):
+        import time
+
+        self._now = time.perf_counter
+        self.t = self._now()
+        self.phases = {}
+
+    def mark(self, name):
+        torch.cuda.synchronize()
+        now = self._now()
+        self.phases[name] = round(self.phases.get(name, 0.0) + now - self.t, 4)
+        self.t = now
+
+
 def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
     dev = gpuplan._dev()
+    tm = PhaseTimer()
     m = gpuplan.single_mapping(mesh, kernel)
     if m is None:
         raise KernelSpecError(f"kernel {kernel.name!r} has no indirect argument to plan")
@@ -184,7 +217,9 @@ def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
     S = config.block_size
     fwd: dict = {}
     map_d = torch.as_tensor(m.table, device=dev).to(torch.int32).reshape(n, m.arity)
+    tm.mark("upload")
     map_d, sizes, meta = _reorder(mesh, kernel, config, m, map_d, fwd)
+    tm.mark("reorder")
 
     if sizes is None:  # chunk_partition (partition.py:165-170)
         offsets = np.append(np.arange(0, n, S, dtype=np.int64), n) if n else np.zeros(1, dtype=np.int64)
@@ -207,7 +242,9 @@ def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
     w_ids_h = wr_ids.to(torch.int64).cpu().numpy()
     w_ptr_h = wr_off.to(torch.int64).cpu().numpy()
     total_pts = int(w_ids_h.max()) + 1 if w_ids_h.size else 1
+    tm.mark("written_lists")
     block_colours = colour_csr_least_loaded(w_ptr_h, w_ids_h, total_pts)
+    tm.mark("block_colouring")
 
     # thread colouring + intra-block colour sort (plan.py:508-522)
     cols, tcounts, sorted_order = gpuplan.thread_colours(bo_d, map_d, wmask, max_block)
@@ -216,6 +253,7 @@ def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
     if n and not torch.equal(so, torch.arange(n, device=dev)):
         map_d = map_d[so]
         _compose(fwd, iter_set, _fwd_from_order(so))
+    tm.mark("thread_colouring")
 
     # staging lists on the final numbering (the sort is intra-block: written lists are unchanged)
     if smask == wmask:
@@ -242,7 +280,9 @@ def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
 
     layouts = _layouts(mesh, kernel, config)
     _iter_identity(fwd, iter_set, n, dev)
+    tm.mark("staging_lists")
     pmesh, perms = _materialise(mesh, kernel, m, map_d, fwd, layouts)
+    tm.mark("host_plan_mesh")
     plan = HierarchicalPlan(
         pmesh, kernel.signature_key(), config, hw, perms, offsets, block_colours,
         tcol_sorted.to(torch.int64).cpu().numpy(), tcounts.to(torch.int64).cpu().numpy(), staged, written,
@@ -252,5 +292,7 @@ def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
         map_d.contiguous(), offsets, block_colours.colours, block_colours.num_colours, tcol_sorted, tcounts,
         st_off, st_ids, wr_off, wr_ids, smask, config.staging == "all-indirect", m.to_set.size, max_block,
     )
+    tm.mark("device_plan")
     object.__setattr__(plan, "_device", dp)
+    object.__setattr__(plan, "_timings", tm.phases)
     return plan

@@ -62,6 +62,17 @@ __device__ __forceinline__ void cpa(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr(dst)), "l"(src) : "memory");
 }
 
+// TMA bulk copy global -> shared, completing bytes on an mbarrier transaction count
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, int bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, int bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+
 constexpr int vbytes(int row_bytes) { return row_bytes % 16 == 0 ? 16 : (row_bytes % 8 == 0 ? 8 : 4); }
 constexpr int align16(int x) { return (x + 15) & ~15; }
 
@@ -91,15 +102,15 @@ struct StageLayout {
   __host__ __device__ StageLayout(int max_staged, int max_block, bool stage_reads) {
     const int qrows = RC == 0 ? 0 : (stage_reads ? max_staged : max_block * A);  // staged or per (elem, slot)
     q_rows = qrows;
-    dir_pitch = max_block + 8;  // + alignment slack (copies start at a 16 B boundary)
+    dir_pitch = ((max_block + 8) + 3) & ~3;  // + alignment slack; pitch bytes stay 16-B multiples
     hdr = 0;
     ids = 64;
     rows_q = align16(ids + max_staged * 4);
     rows_r = align16(rows_q + qrows * RC * (int)sizeof(T));
     slots = align16(rows_r + max_staged * IC * (int)sizeof(T));
-    dir = align16(slots + max_block * A * (int)sizeof(SlotT) + 16);
+    dir = align16(slots + max_block * A * (int)sizeof(SlotT) + 32);
     tc = align16(dir + DC * dir_pitch * (int)sizeof(T));
-    bytes = align16(tc + max_block + 16);
+    bytes = align16(tc + max_block + 32);
   }
 };
 
@@ -137,7 +148,7 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
     // ids already in shared memory.  Claims happen in fill order, which is the
     // order the consumers drain the stages (required by the dataflow proof).
     int* ring = reinterpret_cast<int*>(stage0 + NSTAGE * L.bytes);  // [2][max_staged] ids
-    int* mring = ring + 2 * H.max_staged;                          // [2][max_block*A] map rows
+    int* mring = ring + 2 * ((H.max_staged + 11) & ~3);            // [2][max_block*A] map rows
     const bool map_rows = RC > 0 && !H.stage_reads;
     auto claim = [&](int f) -> int {
       if constexpr (DATAFLOW) return lane == 0 ? (int)atomicAdd(&H.tickets[0], 1u) : 0;
@@ -147,10 +158,12 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
       if constexpr (DATAFLOW) raw = __shfl_sync(0xffffffffu, raw, 0);
       return (raw >= 0 && raw < H.list_len) ? __ldg(H.list + raw) : -1;
     };
+    const int rpitch = (H.max_staged + 11) & ~3;  // 16-B multiple, + window slack
     auto prefetch_ids = [&](int f, int bb, int4 m) {
       if (bb < 0) return;
-      int* dst = ring + (f & 1) * H.max_staged;
-      for (int j = lane; j < m.w; j += 32) cpa<4>(dst + j, H.staged_ids + m.z + j);
+      int* dst = ring + (f & 1) * rpitch;  // 16-B window starting at (s0 & ~3)
+      const int lo = m.z & ~3, nchunk = ((m.z & 3) + m.w + 3) >> 2;
+      for (int j = lane; j < nchunk; j += 32) cpa<16>(dst + 4 * j, H.staged_ids + lo + 4 * j);
       if (map_rows) {
         int* md = mring + (f & 1) * H.max_block * A;
         for (int j = lane; j < m.y * A; j += 32) cpa<4>(md + j, v.map + (int64_t)m.x * A + j);
@@ -186,41 +199,44 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
         break;
       }
       const int e0 = md.x, k = md.y, ns = md.w;
-      // element-local data: slots, direct planes, colours (aligned-down 4 B copies)
-      const int64_t sl_lo = ((int64_t)e0 * A * (int)sizeof(SlotT)) & ~int64_t(3);
-      const int sl_delta = (int)((int64_t)e0 * A * (int)sizeof(SlotT) - sl_lo);
-      const int sl_words = (sl_delta + k * A * (int)sizeof(SlotT) + 3) >> 2;
-      for (int i = lane; i < sl_words; i += 32)
-        cpa<4>(st + L.slots + 4 * i, H.local_slots + sl_lo + 4 * i);
-      const int64_t tc_lo = (int64_t)e0 & ~int64_t(3);
-      const int tc_delta = (int)(e0 - tc_lo);
-      const int tc_words = (tc_delta + k + 3) >> 2;
-      for (int i = lane; i < tc_words; i += 32) cpa<4>(st + L.tc + 4 * i, H.tcol + tc_lo + 4 * i);
-      constexpr int DW = (int)sizeof(T) >= 4 ? 1 : 4 / (int)sizeof(T);
-      const int64_t d_lo = (int64_t)e0 & ~int64_t(DW - 1);
-      const int d_delta = (int)(e0 - d_lo);
-      for (int c = 0; c < DC; ++c) {
-        const T* src = v.dir + (int64_t)c * v.n + d_lo;
-        T* dst = reinterpret_cast<T*>(st + L.dir) + c * L.dir_pitch;
-        const int nel = d_delta + k;
-        if constexpr (sizeof(T) >= 4) {
-          for (int i = lane; i < nel; i += 32) cpa<(int)sizeof(T)>(dst + i, src + i);
-        }
-      }
+      // element-local data: one TMA bulk copy per contiguous piece (16-B windows)
+      int sl_delta = 0, tc_delta = 0;
       if (lane == 0) {
+        const int64_t sb = (int64_t)e0 * A * (int)sizeof(SlotT), slo = sb & ~int64_t(15);
+        sl_delta = (int)(sb - slo);
+        const int sbytes = align16(sl_delta + k * A * (int)sizeof(SlotT));
+        const int64_t tlo = (int64_t)e0 & ~int64_t(15);
+        tc_delta = (int)(e0 - tlo);
+        const int tbytes = align16(tc_delta + k);
+        mbar_expect_tx(&full[s], sbytes + tbytes);
+        bulk_g2s(st + L.slots, H.local_slots + slo, sbytes, &full[s]);
+        bulk_g2s(st + L.tc, H.tcol + tlo, tbytes, &full[s]);
+        const int64_t dir_total = (int64_t)v.dir_comps * v.n * (int)sizeof(T);
+        for (int c = 0; c < DC; ++c) {
+          const int64_t ob = ((int64_t)c * v.n + e0) * (int)sizeof(T), olo = ob & ~int64_t(15);
+          const int dbytes = align16((int)(ob - olo) + k * (int)sizeof(T));
+          T* dst = reinterpret_cast<T*>(st + L.dir) + c * L.dir_pitch;
+          if (olo + dbytes <= dir_total) {
+            hdr[9 + c] = (int)(ob - olo) / (int)sizeof(T);
+            mbar_expect_tx(&full[s], dbytes);
+            bulk_g2s(dst, reinterpret_cast<const unsigned char*>(v.dir) + olo, dbytes, &full[s]);
+          } else {  // tail of the array: element copies (no over-read)
+            hdr[9 + c] = 0;
+            for (int i = 0; i < k; ++i) cpa<(int)sizeof(T)>(dst + i, v.dir + (int64_t)c * v.n + e0 + i);
+          }
+        }
         hdr[0] = b;
         hdr[1] = e0;
         hdr[2] = k;
         hdr[3] = ns;
         hdr[4] = nc0;
         hdr[5] = sl_delta;
-        hdr[6] = d_delta;
         hdr[7] = tc_delta;
       }
       // staged ids (prefetched a fill ago) -> stage; gathers of the staged rows
       asm volatile("cp.async.wait_group 2;" ::: "memory");  // this block's ids have landed
       __syncwarp();
-      const int* rids = ring + (fill & 1) * H.max_staged;
+      const int* rids = ring + (fill & 1) * rpitch + (md.z & 3);
       const int* rmap = mring + (fill & 1) * H.max_block * A;
       int* ids = reinterpret_cast<int*>(st + L.ids);
       T* rq = reinterpret_cast<T*>(st + L.rows_q);
@@ -237,17 +253,43 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
         inc_rows = __all_sync(0xffffffffu, done);
         if (lane == 0) hdr[8] = inc_rows ? 0 : 1;
       }
-      for (int j = lane; j < ns; j += 32) {
-        const int p = rids[j];
-        ids[j] = p;
+      constexpr bool BULK_R = LAYOUT == MP_AOS && (IC * (int)sizeof(T)) % 16 == 0;
+      constexpr bool BULK_Q_T = LAYOUT == MP_AOS && RC > 0 && (RC * (int)sizeof(T)) % 16 == 0;
+      const bool bulk_q = BULK_Q_T && H.stage_reads && v.ind_comps == RC;
+      for (int base = 0; base < ns; base += 32) {
+        const int j = base + lane;
+        const bool valid = j < ns;
+        const int p = valid ? rids[j] : 0;
+        if (valid) ids[j] = p;
+        // runs of consecutive ids -> one bulk copy per run and array
+        const int prev = __shfl_up_sync(0xffffffffu, p, 1);
+        const bool start = valid && (lane == 0 || p != prev + 1);
+        const unsigned mask = __ballot_sync(0xffffffffu, start);
+        if (start && (BULK_R || bulk_q)) {
+          const unsigned above = lane == 31 ? 0u : (mask & ~((2u << lane) - 1u));
+          const int lim = ns - base < 32 ? ns - base : 32;
+          const int len = (above ? __ffs(above) - 1 : lim) - lane;
+          if (BULK_R && inc_rows) {
+            const int bytes = len * IC * (int)sizeof(T);
+            mbar_expect_tx(&full[s], bytes);
+            bulk_g2s(rr + j * IC, v.inc + (int64_t)p * IC, bytes, &full[s]);
+          }
+          if (bulk_q) {
+            const int bytes = len * RC * (int)sizeof(T);
+            mbar_expect_tx(&full[s], bytes);
+            bulk_g2s(rq + j * RCN, v.ind + (int64_t)p * RC, bytes, &full[s]);
+          }
+        }
+        if (!valid) continue;
         if constexpr (LAYOUT == MP_AOS) {
-          constexpr int VR = vbytes(IC * (int)sizeof(T));
+          if (!BULK_R && inc_rows) {
+            constexpr int VR = vbytes(IC * (int)sizeof(T));
 #pragma unroll
-          for (int ch = 0; ch < IC * (int)sizeof(T) / VR; ++ch)
-            if (inc_rows)
+            for (int ch = 0; ch < IC * (int)sizeof(T) / VR; ++ch)
               cpa<VR>(reinterpret_cast<unsigned char*>(rr + j * IC) + ch * VR,
                       reinterpret_cast<const unsigned char*>(v.inc + (int64_t)p * IC) + ch * VR);
-          if (RC > 0 && H.stage_reads) {
+          }
+          if (RC > 0 && H.stage_reads && !bulk_q) {
             constexpr int RCB = RC > 0 ? RC : 1;
             constexpr int VQ = vbytes(RCB * (int)sizeof(T));
             if ((v.ind_comps * (int)sizeof(T)) % VQ == 0) {
@@ -312,9 +354,9 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
 #pragma unroll
         for (int q = 0; q < A; ++q) ls[q] = sl[q];
         T d[DC];
-        const T* dir = reinterpret_cast<const T*>(st + L.dir) + hdr[6] + t;
+        const T* dir = reinterpret_cast<const T*>(st + L.dir) + t;
 #pragma unroll
-        for (int c = 0; c < DC; ++c) d[c] = dir[c * L.dir_pitch];
+        for (int c = 0; c < DC; ++c) d[c] = dir[c * L.dir_pitch + hdr[9 + c]];
         T r[A][RCN];
         if (RC > 0) {
           if (stage_reads) {
@@ -393,7 +435,7 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
 template <class Op, typename T, int LAYOUT, typename SlotT>
 mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
   const StageLayout<Op, T, SlotT> L(P.max_staged, P.block_size, P.stage_reads != 0);
-  const size_t ring = (size_t)2 * P.max_staged * 4 + (size_t)2 * P.block_size * Op::ARITY * 4;
+  const size_t ring = (size_t)2 * ((P.max_staged + 11) & ~3) * 4 + (size_t)2 * P.block_size * Op::ARITY * 4;
   const size_t smem =
       128 + ((P.max_staged * Op::IC * sizeof(T) + 15) & ~size_t(15)) + (size_t)NSTAGE * L.bytes + ring;
   if (smem > 227 * 1024)

@@ -344,6 +344,9 @@ def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sort
     ls = torch.cat([ls, torch.zeros(16 // ls.element_size(), dtype=ls.dtype, device=dev)])
     tcol_sorted_d = torch.cat([tcol_sorted_d.to(torch.uint8), torch.zeros(16, dtype=torch.uint8, device=dev)])
     wsame = bool(torch.equal(st_off, wr_off) and torch.equal(st_ids, wr_ids))
+    pad4 = torch.zeros(4, dtype=torch.int32, device=dev)  # 16-B window over-read slack (pipelined producer)
+    st_ids = torch.cat([st_ids, pad4])
+    wr_ids = st_ids if wsame else torch.cat([wr_ids, pad4])
     meta = torch.stack([bo[:-1], bo[1:] - bo[:-1], st_off[:-1], counts], dim=1).to(torch.int32).contiguous()
     bc = torch.as_tensor(block_colours_np.astype(np.int32), device=dev)
     by_colour = np.lexsort((np.arange(nb), block_colours_np)).astype(np.int32) if nb else np.zeros(0, np.int32)

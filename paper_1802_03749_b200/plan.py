@@ -25,7 +25,7 @@ from .permutation import Permutation
 
 PLAN_HEADER = "meshplan-plan 1"
 STRATEGIES = ("global", "hier")
-REORDER_MODES = ("none", "gps", "partition")
+REORDER_MODES = ("none", "gps", "partition", "cluster")  # "cluster": GPU extension (cluster.py)
 STAGING_MODES = ("all-indirect", "increment-only")
 MAPPING_ENTRY_BYTES = 4  # device mapping entries are int32
 

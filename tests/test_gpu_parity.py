@@ -221,6 +221,35 @@ def test_medium_meshes_all_strategies_exact(family, dims, kname):
     assert np.array_equal(got, counts[:, None] * np.ones((1, got.shape[1]), dtype=got.dtype))
 
 
+@pytest.mark.parametrize("family,dims,kname,bs", [
+    ("quad2d", (96, 80), "flux", 128),
+    ("tri2d", (60, 50), "flux", 96),
+    ("hex3d-nodes", (12, 10, 14), "scatter8", 128),
+    ("hex3d-faces", (10, 9, 8), "face-flux", 64),
+])
+def test_cluster_reorder_plans_are_valid_and_exact(family, dims, kname, bs):
+    """The GPU clustering blocking (extension): widths <= S, race-free (checked
+    on execute), every schedule exact vs serial, reuse at least GPS's."""
+    from oracle import loops
+
+    mesh = mp.generate_mesh(family, dims, dtype="i64")
+    kernel = mp.kernel_for_mesh(kname, mesh)
+    inc = INC_OF[kname]
+    m = next(iter(mesh.mappings.values()))
+    read = {"flux": "q", "face-flux": "state"}.get(kname)
+    direct = {"flux": "w", "scatter8": "stress", "face-flux": "facew"}[kname]
+    want = loops.serial_loop(kname, m.table, None if read is None else mesh.data[read].view2d(),
+                             np.ascontiguousarray(mesh.data[direct].view2d()), _v2(mesh, inc))
+    staging = "increment-only" if kname == "face-flux" else "all-indirect"
+    plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="cluster", block_size=bs, staging=staging))
+    assert plan.working_threads().max() <= bs
+    for sched in SCHEDULES:
+        res, _ = mp.execute_hierarchical(plan, kernel, schedule=sched)
+        assert np.array_equal(_v2(plan.restore_data(res), inc), want), sched
+    gps = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps", block_size=bs, staging=staging))
+    assert mp.reuse_factor(plan) >= 0.95 * mp.reuse_factor(gps)
+
+
 def test_dataflow_repeated_runs_accumulate_exactly():
     """Epoch-stamped flags: many back-to-back dataflow runs stay exact."""
     mesh = mp.generate_mesh("quad2d", (128, 100), dtype="f64")

@@ -35,7 +35,11 @@ def main():
                         block_size=args.block_size)
     t0 = time.perf_counter()
     plan = (mp.build_global_plan if args.strategy == "global" else mp.build_hierarchical_plan)(mesh, kernel, cfg)
-    print(f"plan {time.perf_counter() - t0:.2f}s", flush=True)
+    print(f"plan {time.perf_counter() - t0:.2f}s {getattr(plan, '_timings', '')}", flush=True)
+    if args.strategy == "hier":
+        print(f"blocks {plan.num_blocks} block colours {plan.block_colours.num_colours} "
+              f"reuse {mp.reuse_factor(plan):.3f} thread colours mean {plan.thread_colour_counts.mean():.2f}",
+              flush=True)
     ub = mp.useful_bytes(kernel, mesh)
     scheds = args.schedule.split(",")
     lags = [int(x) for x in args.lags.split(",")] if args.lags else [None]
