@@ -117,7 +117,8 @@ def _materialise(mesh: Mesh, kernel, m: Mapping, map_d: torch.Tensor, fwd: dict,
     inv = {name: _fwd_from_order(f) for name, f in fwd.items()}  # inverse of a forward perm
     perms = {}
     for name, s in mesh.sets.items():
-        perms[name] = Permutation.from_forward(fwd[name].cpu().numpy()) if name in fwd else Permutation.identity(s.size)
+        perms[name] = (Permutation.unchecked(fwd[name].cpu().numpy(), inv[name].cpu().numpy()) if name in fwd
+                       else Permutation.identity(s.size))
     maps = []
     for mm in mesh.mappings.values():
         if mm is m:

@@ -31,6 +31,7 @@ namespace mp {
 namespace {
 
 constexpr int NSTAGE = 3;
+constexpr int PIPE_K = 3;  // staged-id prefetch distance (fills)
 
 __device__ __forceinline__ unsigned saddr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -141,56 +142,81 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
 
   if (warp == 0) {
     // ------------------------------- producer -------------------------------
-    // A 4-deep software pipeline hides the dependent chain claim -> block id ->
-    // descriptor -> staged ids: at fill f the warp claims block f+4, resolves
-    // the id of f+3, loads the descriptor of f+2 and prefetches (cp.async) the
-    // staged ids of f+1 into a 2-slot ring, then gathers block f's rows with
-    // ids already in shared memory.  Claims happen in fill order, which is the
-    // order the consumers drain the stages (required by the dataflow proof).
-    int* ring = reinterpret_cast<int*>(stage0 + NSTAGE * L.bytes);  // [2][max_staged] ids
-    int* mring = ring + 2 * ((H.max_staged + 11) & ~3);            // [2][max_block*A] map rows
+    // Descriptor batches + a K-deep staged-id ring keep every dependent load
+    // (claim -> block id -> descriptor -> staged ids) many fills ahead of its
+    // use: lane i of a batch resolves fill (base + i); the next batch is
+    // issued when the current one starts; the staged ids of fill f+K are
+    // cp.async'd into the ring at fill f.  Claims are taken in fill order,
+    // which is the order the consumers drain the stages (dataflow proof).
+    constexpr int K = PIPE_K, R = PIPE_K + 1;
+    constexpr int BATCH = DATAFLOW ? 8 : 32;
+    const int rpitch = (H.max_staged + 11) & ~3;                      // 16-B multiple + window slack
+    int* ring = reinterpret_cast<int*>(stage0 + NSTAGE * L.bytes);   // [R][rpitch] staged ids
+    int* mring = ring + R * rpitch;                                  // [R][max_block*A] map rows
     const bool map_rows = RC > 0 && !H.stage_reads;
-    auto claim = [&](int f) -> int {
-      if constexpr (DATAFLOW) return lane == 0 ? (int)atomicAdd(&H.tickets[0], 1u) : 0;
-      else return blockIdx.x + f * gridDim.x;
+    auto load_batch = [&](int base, int& bb, int4& mdd, int& ncc) {
+      int raw;
+      if constexpr (DATAFLOW) {
+        int t0 = 0;
+        if (lane == 0) t0 = (int)atomicAdd(&H.tickets[0], (unsigned)BATCH);
+        t0 = __shfl_sync(0xffffffffu, t0, 0);
+        raw = lane < BATCH ? t0 + lane : 0x7fffffff;
+      } else {
+        raw = blockIdx.x + (base + lane) * gridDim.x;
+      }
+      bb = (raw >= 0 && raw < H.list_len) ? __ldg(H.list + raw) : -1;
+      mdd = bb >= 0 ? __ldg(H.meta + bb) : make_int4(0, 0, 0, 0);
+      ncc = bb >= 0 ? __ldg(H.ncol + bb) : 0;
     };
-    auto resolve = [&](int raw) -> int {
-      if constexpr (DATAFLOW) raw = __shfl_sync(0xffffffffu, raw, 0);
-      return (raw >= 0 && raw < H.list_len) ? __ldg(H.list + raw) : -1;
+    int cb, cnc, xb, xnc, cbase = 0;
+    int4 cmd, xmd;
+    load_batch(0, cb, cmd, cnc);
+    load_batch(BATCH, xb, xmd, xnc);
+    auto get = [&](int f, int& bb, int4& mdd, int& ncc) {  // f in [cbase, cbase + 2*BATCH)
+      const int rel = f - cbase;
+      const bool cur = rel < BATCH;
+      const int src = cur ? rel : rel - BATCH;
+      bb = __shfl_sync(0xffffffffu, cur ? cb : xb, src);
+      mdd.x = __shfl_sync(0xffffffffu, cur ? cmd.x : xmd.x, src);
+      mdd.y = __shfl_sync(0xffffffffu, cur ? cmd.y : xmd.y, src);
+      mdd.z = __shfl_sync(0xffffffffu, cur ? cmd.z : xmd.z, src);
+      mdd.w = __shfl_sync(0xffffffffu, cur ? cmd.w : xmd.w, src);
+      ncc = __shfl_sync(0xffffffffu, cur ? cnc : xnc, src);
     };
-    const int rpitch = (H.max_staged + 11) & ~3;  // 16-B multiple, + window slack
-    auto prefetch_ids = [&](int f, int bb, int4 m) {
+    auto prefetch_ids = [&](int f) {
+      int bb, ncc;
+      int4 m;
+      get(f, bb, m, ncc);
       if (bb < 0) return;
-      int* dst = ring + (f & 1) * rpitch;  // 16-B window starting at (s0 & ~3)
+      int* dst = ring + (f % R) * rpitch;  // 16-B window starting at (s0 & ~3)
       const int lo = m.z & ~3, nchunk = ((m.z & 3) + m.w + 3) >> 2;
       for (int j = lane; j < nchunk; j += 32) cpa<16>(dst + 4 * j, H.staged_ids + lo + 4 * j);
       if (map_rows) {
-        int* md = mring + (f & 1) * H.max_block * A;
+        int* md = mring + (f % R) * H.max_block * A;
         for (int j = lane; j < m.y * A; j += 32) cpa<4>(md + j, v.map + (int64_t)m.x * A + j);
       }
     };
-    int raw1 = claim(0), raw2 = claim(1), raw3 = claim(2), raw4 = claim(3);
-    int b0 = resolve(raw1), b1 = resolve(raw2), b2 = resolve(raw3);
-    int4 md0 = b0 >= 0 ? __ldg(H.meta + b0) : make_int4(0, 0, 0, 0);
-    int4 md1 = b1 >= 0 ? __ldg(H.meta + b1) : make_int4(0, 0, 0, 0);
-    int nc0 = b0 >= 0 ? __ldg(H.ncol + b0) : 0;
-    int nc1 = b1 >= 0 ? __ldg(H.ncol + b1) : 0;
-    prefetch_ids(0, b0, md0);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");  // empty "rows" group keeps the wait depth uniform
+    for (int j = 0; j < K; ++j) {
+      prefetch_ids(j);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");  // empty "rows" group: uniform wait depth
+    }
     for (int fill = 0;; ++fill) {
       const int s = fill % NSTAGE;
       unsigned char* st = stage0 + s * L.bytes;
       int* hdr = reinterpret_cast<int*>(st);
-      const int b = b0;
-      const int4 md = md0;
-      // advance the pipeline (results are consumed one fill later)
-      prefetch_ids(fill + 1, b1, md1);
+      if (fill - cbase == BATCH) {  // advance the batches; the next one lands while this one drains
+        cb = xb;
+        cmd = xmd;
+        cnc = xnc;
+        cbase += BATCH;
+        load_batch(cbase + BATCH, xb, xmd, xnc);
+      }
+      prefetch_ids(fill + K);
       asm volatile("cp.async.commit_group;" ::: "memory");
-      const int4 md2 = b2 >= 0 ? __ldg(H.meta + b2) : make_int4(0, 0, 0, 0);
-      const int nc2 = b2 >= 0 ? __ldg(H.ncol + b2) : 0;
-      const int b3 = resolve(raw4);
-      const int raw5 = claim(fill + 4);
+      int b, nc0;
+      int4 md;
+      get(fill, b, md, nc0);
       mbar_wait(&empty[s], ((fill / NSTAGE) & 1) ^ 1);
       if (b < 0) {
         if (lane == 0) hdr[0] = -1;
@@ -233,11 +259,11 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
         hdr[5] = sl_delta;
         hdr[7] = tc_delta;
       }
-      // staged ids (prefetched a fill ago) -> stage; gathers of the staged rows
-      asm volatile("cp.async.wait_group 2;" ::: "memory");  // this block's ids have landed
+      // staged ids (prefetched K fills ago) -> stage; gathers of the staged rows
+      asm volatile("cp.async.wait_group %0;" ::"n"(2 * PIPE_K) : "memory");  // this block's ids have landed
       __syncwarp();
-      const int* rids = ring + (fill & 1) * rpitch + (md.z & 3);
-      const int* rmap = mring + (fill & 1) * H.max_block * A;
+      const int* rids = ring + (fill % R) * rpitch + (md.z & 3);
+      const int* rmap = mring + (fill % R) * H.max_block * A;
       int* ids = reinterpret_cast<int*>(st + L.ids);
       T* rq = reinterpret_cast<T*>(st + L.rows_q);
       T* rr = reinterpret_cast<T*>(st + L.rows_r);
@@ -322,15 +348,6 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
       mbar_arrive(&full[s]);          // releases the header / ids stores
       mbar_arrive_cpasync(&full[s]);  // fires when this lane's copies land
       asm volatile("cp.async.commit_group;" ::: "memory");
-      // rotate the pipeline registers
-      b0 = b1;
-      b1 = b2;
-      b2 = b3;
-      md0 = md1;
-      md1 = md2;
-      nc0 = nc1;
-      nc1 = nc2;
-      raw4 = raw5;
     }
   } else {
     // ------------------------------- consumers ------------------------------
@@ -435,7 +452,7 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
 template <class Op, typename T, int LAYOUT, typename SlotT>
 mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
   const StageLayout<Op, T, SlotT> L(P.max_staged, P.block_size, P.stage_reads != 0);
-  const size_t ring = (size_t)2 * ((P.max_staged + 11) & ~3) * 4 + (size_t)2 * P.block_size * Op::ARITY * 4;
+  const size_t ring = (size_t)(PIPE_K + 1) * (((P.max_staged + 11) & ~3) * 4 + (size_t)P.block_size * Op::ARITY * 4);
   const size_t smem =
       128 + ((P.max_staged * Op::IC * sizeof(T) + 15) & ~size_t(15)) + (size_t)NSTAGE * L.bytes + ring;
   if (smem > 227 * 1024)
