@@ -41,7 +41,7 @@ CONFIGS = {
     "C5": ("quad2d", (5657, 5657), "flux", "f64", "all-indirect"),
 }
 METRIC = "effective HBM GB/s and ms/iter per indirect loop vs global colouring, 1/2/4/8 GPU"
-SCHEDULES = ("pipelined", "colour", "pipelined-dataflow", "dataflow")
+SCHEDULES = ("pipelined-pull", "pipelined", "colour", "pipelined-dataflow-pull", "pipelined-dataflow", "dataflow")
 L2_BYTES = 126 * 2**20
 
 

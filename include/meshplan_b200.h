@@ -44,7 +44,8 @@ enum {                                                             /* device ele
   MP_OP_FACE_FLUX = 3,       /* bench_kernels.py:210-246                   */
   MP_OP_FACE_FLUX_HEAVY = 4  /* bench_kernels.py:234-237                   */
 };
-enum { MP_SCHED_COLOUR = 0, MP_SCHED_DATAFLOW = 1 };              /* hierarchical schedules */
+enum { MP_SCHED_COLOUR = 0, MP_SCHED_DATAFLOW = 1,                /* hierarchical schedules */
+       MP_SCHED_PULL = 4 };  /* | flag, pipelined executor: pull-list form of the colour loop */
 
 /* One indirect loop bound to device arrays (plan numbering).
  * Indirect arrays (ind_read, inc) use ind_layout; direct arrays are SoA
@@ -103,6 +104,11 @@ typedef struct mp_hier_plan {
   uint32_t* flags;                /* [nb] epoch stamps, zero-initialised     */
   uint32_t* tickets;              /* [2] next-block ticket, finished blocks;
                                      zero-initialised, re-armed by the kernel */
+  /* Pull lists (optional, pipelined executor): for block b and staged row j,
+   * the (element*arity + slot) refs writing row j in thread-colour order are
+   * pull_ref[e0*arity + pull_off[s0 + b + j] .. pull_off[s0 + b + j + 1]). */
+  const uint16_t* pull_off;       /* [staged total + nb] (or NULL)           */
+  const uint16_t* pull_ref;       /* [n_elems*arity]                         */
 } mp_hier_plan;
 
 /* ---- library ------------------------------------------------------------ */

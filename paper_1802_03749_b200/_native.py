@@ -19,7 +19,7 @@ LIB_PATH = Path(os.environ.get("MESHPLAN_B200_LIB", Path(__file__).resolve().par
 
 MP_F64, MP_F32, MP_I64, MP_I32 = 0, 1, 2, 3
 MP_AOS, MP_SOA = 0, 1
-MP_SCHED_COLOUR, MP_SCHED_DATAFLOW = 0, 1
+MP_SCHED_COLOUR, MP_SCHED_DATAFLOW, MP_SCHED_PULL = 0, 1, 4
 OPS = {"flux": 0, "flux-noread": 1, "scatter8": 2, "face-flux": 3, "face-flux-heavy": 4}
 DTYPES = {"f64": MP_F64, "f32": MP_F32, "i64": MP_I64, "i32": MP_I32}
 LAYOUTS = {"aos": MP_AOS, "soa": MP_SOA}
@@ -49,6 +49,7 @@ class MpHierPlan(ctypes.Structure):
         ("num_block_colours", c_i32), ("pad_", c_i32),
         ("colour_block_offsets_host", c_vp), ("blocks_by_colour", c_vp),
         ("order", c_vp), ("pred_offsets", c_vp), ("preds", c_vp), ("flags", c_vp), ("tickets", c_vp),
+        ("pull_off", c_vp), ("pull_ref", c_vp),
     ]
 
 

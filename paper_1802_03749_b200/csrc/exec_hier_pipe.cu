@@ -93,13 +93,15 @@ struct PipeView {
   int32_t stage_reads;
   int32_t max_staged;
   int32_t max_block;
+  const unsigned char* __restrict__ pull_off;  // uint16 per (block, staged row) + 1
+  const unsigned char* __restrict__ pull_ref;  // uint16 per (element, slot)
 };
 
 // Byte layout of one stage, computed identically on host and device.
 template <class Op, typename T, typename SlotT>
 struct StageLayout {
   static constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC;
-  int hdr, ids, rows_q, rows_r, slots, dir, tc, bytes, dir_pitch, q_rows;
+  int hdr, ids, rows_q, rows_r, slots, dir, tc, poff, pref, bytes, dir_pitch, q_rows;
   __host__ __device__ StageLayout(int max_staged, int max_block, bool stage_reads) {
     const int qrows = RC == 0 ? 0 : (stage_reads ? max_staged : max_block * A);  // staged or per (elem, slot)
     q_rows = qrows;
@@ -111,13 +113,22 @@ struct StageLayout {
     slots = align16(rows_r + max_staged * IC * (int)sizeof(T));
     dir = align16(slots + max_block * A * (int)sizeof(SlotT) + 32);
     tc = align16(dir + DC * dir_pitch * (int)sizeof(T));
-    bytes = align16(tc + max_block + 32);
+    poff = align16(tc + max_block + 32);               // pull lists (pull variant)
+    pref = align16(poff + (max_staged + 1) * 2 + 32);
+    bytes = align16(pref + max_block * A * 2 + 32);
   }
 };
 
 // header ints: 0 block (-1: stop), 1 e0, 2 k, 3 ns, 4 ncol, 5 slot byte delta, 6 dir elem delta, 7 tc delta
 
-template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT>
+// Increment buffer: colour-loop variant [max_staged][IC] accumulators;
+// pull variant [A][IC][max_block] per-(element, slot) increments.
+template <class Op, typename T, bool PULL>
+__host__ __device__ inline int inc_buffer_bytes(int max_staged, int max_block) {
+  return align16((PULL ? max_block * Op::ARITY : max_staged) * Op::IC * (int)sizeof(T));
+}
+
+template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, bool PULL>
 __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView H) {
   constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + NSTAGE;
   T* sh_inc = reinterpret_cast<T*>(smem + 128);
-  unsigned char* stage0 = smem + 128 + align16(H.max_staged * IC * (int)sizeof(T));
+  unsigned char* stage0 = smem + 128 + inc_buffer_bytes<Op, T, PULL>(H.max_staged, H.max_block);
   const bool stage_reads = RC > 0 && H.stage_reads;
 
   if (threadIdx.x == 0) {
@@ -137,7 +148,8 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
       mbar_init(&empty[s], 1);
     }
   }
-  for (int i = threadIdx.x; i < H.max_staged * IC; i += nthreads) sh_inc[i] = T(0);
+  if (!PULL)
+    for (int i = threadIdx.x; i < H.max_staged * IC; i += nthreads) sh_inc[i] = T(0);
   __syncthreads();
 
   if (warp == 0) {
@@ -231,12 +243,25 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
         const int64_t sb = (int64_t)e0 * A * (int)sizeof(SlotT), slo = sb & ~int64_t(15);
         sl_delta = (int)(sb - slo);
         const int sbytes = align16(sl_delta + k * A * (int)sizeof(SlotT));
-        const int64_t tlo = (int64_t)e0 & ~int64_t(15);
-        tc_delta = (int)(e0 - tlo);
-        const int tbytes = align16(tc_delta + k);
-        mbar_expect_tx(&full[s], sbytes + tbytes);
+        mbar_expect_tx(&full[s], sbytes);
         bulk_g2s(st + L.slots, H.local_slots + slo, sbytes, &full[s]);
-        bulk_g2s(st + L.tc, H.tcol + tlo, tbytes, &full[s]);
+        if constexpr (PULL) {  // pull lists instead of thread colours
+          const int64_t pob = ((int64_t)md.z + b) * 2, polo = pob & ~int64_t(15);
+          const int pobytes = align16((int)(pob - polo) + (ns + 1) * 2);
+          const int64_t prb = (int64_t)e0 * A * 2, prlo = prb & ~int64_t(15);
+          const int prbytes = align16((int)(prb - prlo) + k * A * 2);
+          hdr[13] = (int)(pob - polo) / 2;
+          hdr[14] = (int)(prb - prlo) / 2;
+          mbar_expect_tx(&full[s], pobytes + prbytes);
+          bulk_g2s(st + L.poff, H.pull_off + polo, pobytes, &full[s]);
+          bulk_g2s(st + L.pref, H.pull_ref + prlo, prbytes, &full[s]);
+        } else {
+          const int64_t tlo = (int64_t)e0 & ~int64_t(15);
+          tc_delta = (int)(e0 - tlo);
+          const int tbytes = align16(tc_delta + k);
+          mbar_expect_tx(&full[s], tbytes);
+          bulk_g2s(st + L.tc, H.tcol + tlo, tbytes, &full[s]);
+        }
         const int64_t dir_total = (int64_t)v.dir_comps * v.n * (int)sizeof(T);
         for (int c = 0; c < DC; ++c) {
           const int64_t ob = ((int64_t)c * v.n + e0) * (int)sizeof(T), olo = ob & ~int64_t(15);
@@ -389,7 +414,62 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
           }
         }
         compute<Op, T>(v, r, d, o);
-        my_tc = (st + L.tc)[hdr[7] + t];
+        if (!PULL) my_tc = (st + L.tc)[hdr[7] + t];
+      }
+      if constexpr (PULL) {
+        // Pull form of the colour loop: every element parks its per-slot
+        // increments (conflict-free, element-fastest layout); one barrier; the
+        // owner of staged row j sums the row's refs in thread-colour order
+        // starting from 0 -- the same additions, in the same order, as the
+        // reference's zeroed shared row + per-colour np.add.at -- and writes
+        // row + sum back once.
+        const int kp = H.max_block;
+        if (t < k) {
+#pragma unroll
+          for (int q = 0; q < A; ++q)
+#pragma unroll
+            for (int c = 0; c < IC; ++c) sh_inc[(q * IC + c) * kp + t] = o[q][c];
+        }
+        named_sync(1, nc_threads);
+        bool late = false;
+        if constexpr (DATAFLOW) {
+          late = hdr[8] != 0;
+          if (late) {
+            const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
+            for (int i = t; i < nq; i += nc_threads) {
+              const uint32_t* f = H.flags + __ldg(H.preds + q0 + i);
+              while (ld_acquire_gpu(f) != H.epoch) __nanosleep(32);
+            }
+            named_sync(1, nc_threads);
+          }
+        }
+        const uint16_t* po = reinterpret_cast<const uint16_t*>(st + L.poff) + hdr[13];
+        const uint16_t* pr = reinterpret_cast<const uint16_t*>(st + L.pref) + hdr[14];
+        for (int j = t; j < ns; j += nc_threads) {
+          T acc[IC];
+#pragma unroll
+          for (int c = 0; c < IC; ++c) acc[c] = T(0);
+          for (int r2 = po[j]; r2 < po[j + 1]; ++r2) {
+            const int ref = pr[r2], te = ref / A, q = ref - te * A;
+#pragma unroll
+            for (int c = 0; c < IC; ++c) acc[c] += sh_inc[(q * IC + c) * kp + te];
+          }
+          const int64_t p = ids[j];
+#pragma unroll
+          for (int c = 0; c < IC; ++c) {
+            T* a = v.inc + ind_index<LAYOUT>(p, c, IC, v.npts);
+            *a = (late ? ld_cg(a) : rr[j * IC + c]) + acc[c];
+          }
+        }
+        named_sync(1, nc_threads);
+        if (t == 0) {
+          if constexpr (DATAFLOW) {
+            __threadfence();
+            st_release_gpu(H.flags + b, H.epoch);
+          }
+          mbar_arrive(&empty[s]);
+        }
+        continue;
       }
       for (int c = 0; c < nc; ++c) {
         if (my_tc == c) {
@@ -449,17 +529,18 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
   }
 }
 
-template <class Op, typename T, int LAYOUT, typename SlotT>
+template <class Op, typename T, int LAYOUT, typename SlotT, bool PULL>
 mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
   const StageLayout<Op, T, SlotT> L(P.max_staged, P.block_size, P.stage_reads != 0);
   const size_t ring = (size_t)(PIPE_K + 1) * (((P.max_staged + 11) & ~3) * 4 + (size_t)P.block_size * Op::ARITY * 4);
   const size_t smem =
-      128 + ((P.max_staged * Op::IC * sizeof(T) + 15) & ~size_t(15)) + (size_t)NSTAGE * L.bytes + ring;
+      128 + inc_buffer_bytes<Op, T, PULL>(P.max_staged, P.block_size) + (size_t)NSTAGE * L.bytes + ring;
   if (smem > 227 * 1024)
     MP_FAIL(MP_ERR_CAPACITY, "pipelined stages need %zu shared bytes, over the 232448-byte limit", smem);
   const int consumers = ((P.block_size + 31) / 32) * 32;
   const int threads = consumers + 32;
-  auto kern = dataflow ? hier_pipe_kernel<Op, T, LAYOUT, true, SlotT> : hier_pipe_kernel<Op, T, LAYOUT, false, SlotT>;
+  auto kern = dataflow ? hier_pipe_kernel<Op, T, LAYOUT, true, SlotT, PULL>
+                       : hier_pipe_kernel<Op, T, LAYOUT, false, SlotT, PULL>;
   MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, dev = 0, sms = 0;
   MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
@@ -488,7 +569,8 @@ mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, b
 }
 
 template <class Op, typename T>
-mp_status launch_pipe_op(const mp_loop& Lp, const mp_hier_plan& P, bool dataflow, uint32_t epoch, cudaStream_t st) {
+mp_status launch_pipe_op(const mp_loop& Lp, const mp_hier_plan& P, bool dataflow, bool pull, uint32_t epoch,
+                         cudaStream_t st) {
   if constexpr (!op_supported<Op, T>()) {
     MP_FAIL(MP_ERR_KERNEL, "heavy face flux needs float data");
   } else {
@@ -497,17 +579,24 @@ mp_status launch_pipe_op(const mp_loop& Lp, const mp_hier_plan& P, bool dataflow
     if (P.num_blocks == 0) return MP_OK;
     if (!P.written_is_staged) MP_FAIL(MP_ERR_KERNEL, "pipelined executor needs written lists equal to staged lists");
     if (P.block_size > 992) MP_FAIL(MP_ERR_CAPACITY, "block size %d exceeds 992 (+1 producer warp)", P.block_size);
+    if (pull && (!P.pull_off || !P.pull_ref)) MP_FAIL(MP_ERR_KERNEL, "pull variant needs the plan's pull lists");
     PipeView H{reinterpret_cast<const int4*>(P.meta), P.staged_ids,
                static_cast<const unsigned char*>(P.local_slots), P.thread_colours, P.colour_counts,
                nullptr, 0, P.pred_offsets, P.preds, P.flags, P.tickets, epoch, P.stage_reads, P.max_staged,
-               P.block_size};
+               P.block_size, reinterpret_cast<const unsigned char*>(P.pull_off),
+               reinterpret_cast<const unsigned char*>(P.pull_ref)};
     LoopView<T> v = make_view<T>(Lp);
     const bool u8 = P.slot_bytes == 1;
-    if (Lp.ind_layout == MP_AOS)
-      return u8 ? launch_pipe<Op, T, MP_AOS, uint8_t>(v, H, P, dataflow, st)
-                : launch_pipe<Op, T, MP_AOS, uint16_t>(v, H, P, dataflow, st);
-    return u8 ? launch_pipe<Op, T, MP_SOA, uint8_t>(v, H, P, dataflow, st)
-              : launch_pipe<Op, T, MP_SOA, uint16_t>(v, H, P, dataflow, st);
+#define MP_PIPE(LAY, SL)                                                                      \
+  return pull ? launch_pipe<Op, T, LAY, SL, true>(v, H, P, dataflow, st)                      \
+              : launch_pipe<Op, T, LAY, SL, false>(v, H, P, dataflow, st);
+    if (Lp.ind_layout == MP_AOS) {
+      if (u8) { MP_PIPE(MP_AOS, uint8_t) }
+      MP_PIPE(MP_AOS, uint16_t)
+    }
+    if (u8) { MP_PIPE(MP_SOA, uint8_t) }
+    MP_PIPE(MP_SOA, uint16_t)
+#undef MP_PIPE
   }
 }
 
@@ -518,12 +607,13 @@ extern "C" mp_status mp_exec_hier_pipelined(const mp_loop* loop, const mp_hier_p
                                             uint32_t epoch, void* stream) {
   mp::clear_error();
   if (!loop || !plan) MP_FAIL(MP_ERR_KERNEL, "null argument");
-  const bool df = schedule == MP_SCHED_DATAFLOW;
+  const bool df = (schedule & 3) == MP_SCHED_DATAFLOW;
+  const bool pull = (schedule & MP_SCHED_PULL) != 0;
   if (df && epoch == 0) MP_FAIL(MP_ERR_KERNEL, "dataflow epochs start at 1");
   cudaStream_t st = mp::as_stream(stream);
   const mp_loop& L = *loop;
   const mp_hier_plan& P = *plan;
   return MP_DISPATCH_OP(L.op, [&]() {
-    return MP_DISPATCH_DTYPE(L.dtype, [&]() { return mp::launch_pipe_op<Op, scalar_t>(L, P, df, epoch, st); });
+    return MP_DISPATCH_DTYPE(L.dtype, [&]() { return mp::launch_pipe_op<Op, scalar_t>(L, P, df, pull, epoch, st); });
   });
 }

@@ -30,6 +30,8 @@ SCHEDULES = {
     "dataflow": (_native.MP_SCHED_DATAFLOW, False),
     "pipelined": (_native.MP_SCHED_COLOUR, True),
     "pipelined-dataflow": (_native.MP_SCHED_DATAFLOW, True),
+    "pipelined-pull": (_native.MP_SCHED_COLOUR | _native.MP_SCHED_PULL, True),
+    "pipelined-dataflow-pull": (_native.MP_SCHED_DATAFLOW | _native.MP_SCHED_PULL, True),
 }
 TORCH_DTYPES = {"f64": torch.float64, "f32": torch.float32, "i64": torch.int64, "i32": torch.int32}
 
@@ -172,7 +174,7 @@ class DeviceLoop:
             _native.call("mp_exec_global", self.loop, offs.ctypes.data, len(offs) - 1,
                          int(self.plan.config.block_size), sp)
         else:
-            if self.schedule == _native.MP_SCHED_DATAFLOW:
+            if self.schedule & 3 == _native.MP_SCHED_DATAFLOW:
                 dp.epoch = dp.epoch % 0xFFFFFFFF + 1  # flags hold the last epoch; never 0
             fn = "mp_exec_hier_pipelined" if self.pipelined else "mp_exec_hier"
             _native.call(fn, self.loop, dp.struct_cached(), self.schedule, max(dp.epoch, 1), sp)
@@ -196,7 +198,7 @@ class DeviceLoop:
     def launches_per_run(self) -> int:
         if isinstance(self.plan, GlobalPlan):
             return int(np.count_nonzero(np.diff(self.plan._device.colour_offsets)))
-        if self.schedule == _native.MP_SCHED_DATAFLOW:
+        if self.schedule & 3 == _native.MP_SCHED_DATAFLOW:
             return 1 if self.plan.num_blocks else 0
         return int(np.count_nonzero(np.diff(self.plan._device.colour_block_offsets)))
 
@@ -395,8 +397,9 @@ def _report(plan, kernel, loop: DeviceLoop, ms: float | None) -> MetricsReport:
         "hier", n, loop.launches_per_run(), plan.block_colours.num_colours, ub, tb, ops, occ, bps,
         reuse_factor(plan), int(plan.thread_colour_counts.max()) if nb else 0,
         float(plan.thread_colour_counts.mean()) if nb else 0.0, int(sync.sum()) if nb else 0, sync, smax, nb,
-        ("pipelined-" if loop.pipelined else "") + ("dataflow" if loop.schedule == _native.MP_SCHED_DATAFLOW
-                                                    else "colour"), ms, gbps,
+        ("pipelined-" if loop.pipelined else "") + ("dataflow" if loop.schedule & 3 == _native.MP_SCHED_DATAFLOW
+                                                    else "colour") + ("-pull" if loop.schedule & 4 else ""),
+        ms, gbps,
     )
 
 

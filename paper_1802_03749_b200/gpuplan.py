@@ -298,6 +298,8 @@ class DevicePlan:
     stage_reads: bool
     written_is_staged: bool
     npts: int
+    pull_off: torch.Tensor | None = None  # int16 (uint16 bits) pull-list offsets
+    pull_ref: torch.Tensor | None = None  # int16 local refs e*arity+s
     lag: int = DATAFLOW_LAG
     epoch: int = 0
 
@@ -318,6 +320,9 @@ class DevicePlan:
             setattr(p, name, t.data_ptr())
         p.num_block_colours = len(self.colour_block_offsets) - 1
         p.colour_block_offsets_host = self.colour_block_offsets.ctypes.data
+        if self.pull_off is not None:
+            p.pull_off = self.pull_off.data_ptr()
+            p.pull_ref = self.pull_ref.data_ptr()
         return p
 
     def reschedule(self, lag: int) -> None:
@@ -329,6 +334,35 @@ class DevicePlan:
         self.__dict__.pop("_struct", None)
 
 
+def pull_lists(bo: torch.Tensor, ls16: torch.Tensor, arity: int, st_off: torch.Tensor, counts: torch.Tensor,
+               max_staged: int):
+    """Per block and staged row, the (element*arity + slot) refs writing the
+    row in thread-colour order (elements are colour-sorted, so (element, slot)
+    order): the pull form of the colour loop (plan.py:508-517 order,
+    simulator.py:634-643 semantics).  None when some slot is not staged."""
+    dev = bo.device
+    nb = bo.numel() - 1
+    n_ref = int(bo[-1]) * arity
+    slot = ls16[:n_ref].long()
+    if nb == 0 or n_ref == 0 or bool((slot < 0).any()):
+        return None, None
+    sizes = (bo[1:] - bo[:-1]).long()
+    ref_block = torch.repeat_interleave(torch.arange(nb, device=dev), sizes * arity)
+    width = max_staged + 1
+    key = ref_block * width + slot
+    order = torch.sort(key, stable=True).indices
+    ref = order - bo.long()[ref_block] * arity  # sorted refs stay inside their block
+    cnt = torch.bincount(key, minlength=nb * width).view(nb, width)
+    excl = torch.cumsum(cnt, 1) - cnt
+    j = torch.arange(width, device=dev)
+    valid = j[None, :] <= counts.long()[:, None]
+    dest = (st_off[:-1].long() + torch.arange(nb, device=dev))[:, None] + j[None, :]
+    off = torch.zeros(int(st_off[-1]) + nb + 8, dtype=torch.int16, device=dev)
+    off[dest[valid]] = excl[valid].to(torch.int16)
+    ref16 = torch.cat([ref.to(torch.int16), torch.zeros(8, dtype=torch.int16, device=dev)])
+    return off, ref16
+
+
 def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sorted_d, tcounts_d, st_off, st_ids,
                       wr_off, wr_ids, stage_mask, stage_reads, npts, block_size) -> DevicePlan:
     """Assemble the executor structures (slots, schedules) from plan arrays."""
@@ -338,6 +372,9 @@ def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sort
     ls, ws = local_slots(bo, map_d, stage_mask, st_off, st_ids, wr_off, wr_ids)
     counts = (st_off[1:] - st_off[:-1]) if nb else torch.zeros(0, dtype=torch.int32, device=dev)
     max_staged = int(counts.max()) if nb else 0
+    arity = map_d.shape[1]
+    full_mask = stage_mask == (1 << arity) - 1
+    p_off, p_ref = pull_lists(bo, ls, arity, st_off, counts, max_staged) if full_mask else (None, None)
     if max_staged <= 256:
         ls = ls.to(torch.uint8)  # slot values < 256 (unused slots 0xFFFF only where not staged)
     # 16 bytes of tail padding: the pipelined producer copies 4-byte aligned windows
@@ -363,7 +400,7 @@ def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sort
         blocks_by_colour=torch.as_tensor(by_colour, device=dev), colour_block_offsets=cbo, order=order,
         pred_off=pred_off, preds=preds, flags=torch.zeros(max(nb, 1), dtype=torch.int32, device=dev),
         tickets=torch.zeros(2, dtype=torch.int32, device=dev), block_size=int(block_size), max_staged=max_staged,
-        stage_reads=bool(stage_reads), written_is_staged=wsame, npts=int(npts),
+        stage_reads=bool(stage_reads), written_is_staged=wsame, npts=int(npts), pull_off=p_off, pull_ref=p_ref,
     )
 
 

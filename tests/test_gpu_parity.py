@@ -18,7 +18,7 @@ from helpers import config_of, reference_plan
 pytestmark = pytest.mark.gpu
 
 CASES = golden_cases()
-SCHEDULES = ("dataflow", "colour", "pipelined", "pipelined-dataflow")
+SCHEDULES = ("dataflow", "colour", "pipelined", "pipelined-dataflow", "pipelined-pull", "pipelined-dataflow-pull")
 
 
 def _ids(c):
