@@ -25,12 +25,14 @@
 // producer only ever waits on smaller tickets, which are either finished,
 // sitting in some stage (consumers never block), or being claimed by a
 // producer that waits on still smaller tickets: no deadlock.
+#include <stdlib.h>
+
 #include "mp_loop.cuh"
 
 namespace mp {
 namespace {
 
-constexpr int NSTAGE = 3;
+constexpr int MAX_STAGES = 8;  // mbarrier pairs that fit the 128-byte header
 constexpr int PIPE_K = 3;  // staged-id prefetch distance (fills)
 
 __device__ __forceinline__ unsigned saddr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -93,6 +95,7 @@ struct PipeView {
   int32_t stage_reads;
   int32_t max_staged;
   int32_t max_block;
+  int32_t nstage;
   const unsigned char* __restrict__ pull_off;  // uint16 per (block, staged row) + 1
   const unsigned char* __restrict__ pull_ref;  // uint16 per (element, slot)
 };
@@ -137,7 +140,8 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
   const int nc_threads = nthreads - 32;  // consumers: warps 1..
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + NSTAGE;
+  uint64_t* empty = full + MAX_STAGES;
+  const int NSTAGE = H.nstage;
   T* sh_inc = reinterpret_cast<T*>(smem + 128);
   unsigned char* stage0 = smem + 128 + inc_buffer_bytes<Op, T, PULL>(H.max_staged, H.max_block);
   const bool stage_reads = RC > 0 && H.stage_reads;
@@ -532,7 +536,13 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
 template <class Op, typename T, int LAYOUT, typename SlotT, bool PULL>
 mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
   const StageLayout<Op, T, SlotT> L(P.max_staged, P.block_size, P.stage_reads != 0);
-  const size_t ring = (size_t)(PIPE_K + 1) * (((P.max_staged + 11) & ~3) * 4 + (size_t)P.block_size * Op::ARITY * 4);
+  const bool map_rows = Op::RC > 0 && !P.stage_reads;
+  const size_t ring = (size_t)(PIPE_K + 1) * (((P.max_staged + 11) & ~3) * 4 +
+                                              (map_rows ? (size_t)P.block_size * Op::ARITY * 4 : 0));
+  static const int env_stages = getenv("MESHPLAN_PIPE_STAGES") ? atoi(getenv("MESHPLAN_PIPE_STAGES")) : 3;
+  static const int env_ctas = getenv("MESHPLAN_PIPE_CTAS") ? atoi(getenv("MESHPLAN_PIPE_CTAS")) : 0;
+  const int NSTAGE = env_stages < 2 ? 2 : (env_stages > MAX_STAGES ? MAX_STAGES : env_stages);
+  H.nstage = NSTAGE;
   const size_t smem =
       128 + inc_buffer_bytes<Op, T, PULL>(P.max_staged, P.block_size) + (size_t)NSTAGE * L.bytes + ring;
   if (smem > 227 * 1024)
@@ -547,6 +557,7 @@ mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, b
   MP_CUDA_TRY(cudaGetDevice(&dev));
   MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (per_sm < 1) MP_FAIL(MP_ERR_CAPACITY, "pipelined executor does not fit on an SM (%zu shared bytes)", smem);
+  if (env_ctas > 0 && env_ctas < per_sm) per_sm = env_ctas;
   const int resident = per_sm * sms;
   if (dataflow) {
     H.list = P.order;
@@ -583,7 +594,7 @@ mp_status launch_pipe_op(const mp_loop& Lp, const mp_hier_plan& P, bool dataflow
     PipeView H{reinterpret_cast<const int4*>(P.meta), P.staged_ids,
                static_cast<const unsigned char*>(P.local_slots), P.thread_colours, P.colour_counts,
                nullptr, 0, P.pred_offsets, P.preds, P.flags, P.tickets, epoch, P.stage_reads, P.max_staged,
-               P.block_size, reinterpret_cast<const unsigned char*>(P.pull_off),
+               P.block_size, 3, reinterpret_cast<const unsigned char*>(P.pull_off),
                reinterpret_cast<const unsigned char*>(P.pull_ref)};
     LoopView<T> v = make_view<T>(Lp);
     const bool u8 = P.slot_bytes == 1;
