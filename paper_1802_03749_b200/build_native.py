@@ -52,7 +52,8 @@ def _compile(src: Path, verbose: bool) -> Path:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed on {src.name}:\n{r.stderr[-6000:]}")
+        err = r.stderr if len(r.stderr) < 8000 else r.stderr[:5000] + "\n...\n" + r.stderr[-3000:]
+        raise RuntimeError(f"nvcc failed on {src.name}:\n{err}")
     if verbose and r.stderr:
         (OBJ_DIR / (src.name + ".ptxas.txt")).write_text(r.stderr)
     return obj
