@@ -109,6 +109,16 @@ typedef struct mp_hier_plan {
    * pull_ref[e0*arity + pull_off[s0 + b + j] .. pull_off[s0 + b + j + 1]). */
   const uint16_t* pull_off;       /* [staged total + nb] (or NULL)           */
   const uint16_t* pull_ref;       /* [n_elems*arity]                         */
+  /* Streamed executor (mp_exec_hier_stream): per-ticket block descriptors
+   * {first element, elements | thread colours << 16, staged offset, staged
+   * count} in blocks_by_colour order and in dataflow order, and one packed
+   * record per element: arity local slots (slot_bytes each), the element's
+   * thread colour (1 byte), zero padding to elem_meta_bytes (multiple of 4). */
+  const int32_t* tdesc_colour;    /* [nb][4]                                 */
+  const int32_t* tdesc_order;     /* [nb][4]                                 */
+  const uint8_t* elem_meta;       /* [n_elems*elem_meta_bytes]               */
+  int32_t elem_meta_bytes;
+  int32_t pad2_;
 } mp_hier_plan;
 
 /* ---- library ------------------------------------------------------------ */
@@ -138,6 +148,16 @@ mp_status mp_exec_hier(const mp_loop* loop, const mp_hier_plan* plan, int32_t sc
  * acquires the predecessors' flags before gathering increment rows. */
 mp_status mp_exec_hier_pipelined(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule, uint32_t epoch,
                                  void* stream);
+
+/* Same semantics and results as mp_exec_hier, as a lean persistent kernel:
+ * every thread both gathers and computes; a D-deep cp.async ring (one commit
+ * group per block) keeps D blocks in flight; descriptor -> staged-id -> row
+ * loads are software-pipelined in registers; shared rows use a
+ * bank-conflict-free odd-granule pitch.  MP_SCHED_DATAFLOW adds a sync warp
+ * per CTA that checks predecessors ahead of use and releases finished blocks
+ * in batches.  Needs written_is_staged, tdesc_* and elem_meta. */
+mp_status mp_exec_hier_stream(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule, uint32_t epoch,
+                              void* stream);
 
 /* execute_serial (simulator.py:215-230) on the device: per-element
  * increments to a temp array, then per point an ordered sum over its

@@ -50,6 +50,8 @@ class MpHierPlan(ctypes.Structure):
         ("colour_block_offsets_host", c_vp), ("blocks_by_colour", c_vp),
         ("order", c_vp), ("pred_offsets", c_vp), ("preds", c_vp), ("flags", c_vp), ("tickets", c_vp),
         ("pull_off", c_vp), ("pull_ref", c_vp),
+        ("tdesc_colour", c_vp), ("tdesc_order", c_vp), ("elem_meta", c_vp), ("elem_meta_bytes", c_i32),
+        ("pad2_", c_i32),
     ]
 
 
@@ -60,6 +62,7 @@ _SIGNATURES = {
     "mp_exec_global": (c_i32, [ctypes.POINTER(MpLoop), c_vp, c_i32, c_i32, c_vp]),
     "mp_exec_hier": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_u32, c_vp]),
     "mp_exec_hier_pipelined": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_u32, c_vp]),
+    "mp_exec_hier_stream": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_u32, c_vp]),
     "mp_exec_serial":(c_i32, [ctypes.POINTER(MpLoop), c_vp, c_vp, c_vp, c_vp]),
     "mp_race_check": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "mp_plan_block_points": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_i32, c_u32, c_i32, c_vp, c_vp, c_vp, c_vp]),

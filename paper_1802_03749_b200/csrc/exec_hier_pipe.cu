@@ -18,13 +18,15 @@
 //     colour at a time (named barrier among consumer warps only), write
 //     row + increment back once, and release the stage.
 //
-// Dataflow schedule: the producer checks the block's lower-colour
-// predecessors' flags (acquire) before gathering the increment rows, so the
-// rows it prefetches already contain every earlier writer's contribution;
-// consumers never wait.  Tickets are claimed in a topological order, so a
-// producer only ever waits on smaller tickets, which are either finished,
-// sitting in some stage (consumers never block), or being claimed by a
-// producer that waits on still smaller tickets: no deadlock.
+// Dataflow schedule: one launch; CTA i takes tickets i, i+grid, i+2*grid, ...
+// of a topological order of the lower-colour conflict DAG (static claims, no
+// ticket atomics).  Before gathering a block's increment rows the producer
+// waits (acquire) for the block's lower-colour predecessors, so the rows it
+// prefetches already hold every earlier writer's contribution and consumers
+// never wait.  A producer only waits on smaller tickets, and the CTA holding
+// the smallest unfinished ticket has finished all its earlier ones, so that
+// ticket always progresses: no deadlock while every CTA is resident (the grid
+// is capped at the occupancy-derived resident count).
 #include <stdlib.h>
 
 #include "mp_loop.cuh"
@@ -165,22 +167,17 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
     // cp.async'd into the ring at fill f.  Claims are taken in fill order,
     // which is the order the consumers drain the stages (dataflow proof).
     constexpr int K = PIPE_K, R = PIPE_K + 1;
-    constexpr int BATCH = DATAFLOW ? 8 : 32;
+    constexpr int BATCH = 32;
     const int rpitch = (H.max_staged + 11) & ~3;                      // 16-B multiple + window slack
     int* ring = reinterpret_cast<int*>(stage0 + NSTAGE * L.bytes);   // [R][rpitch] staged ids
     int* mring = ring + R * rpitch;                                  // [R][max_block*A] map rows
     const bool map_rows = RC > 0 && !H.stage_reads;
     auto load_batch = [&](int base, int& bb, int4& mdd, int& ncc) {
-      int raw;
-      if constexpr (DATAFLOW) {
-        int t0 = 0;
-        if (lane == 0) t0 = (int)atomicAdd(&H.tickets[0], (unsigned)BATCH);
-        t0 = __shfl_sync(0xffffffffu, t0, 0);
-        raw = lane < BATCH ? t0 + lane : 0x7fffffff;
-      } else {
-        raw = blockIdx.x + (base + lane) * gridDim.x;
-      }
-      bb = (raw >= 0 && raw < H.list_len) ? __ldg(H.list + raw) : -1;
+      // static round-robin claims (both schedules): fill f of CTA i takes list
+      // entry i + f * grid -- no ticket atomics, and on the dataflow schedule
+      // the claimed-but-unfinished window stays ~grid * NSTAGE tickets wide
+      const int raw = blockIdx.x + (base + lane) * gridDim.x;
+      bb = raw < H.list_len ? __ldg(H.list + raw) : -1;
       mdd = bb >= 0 ? __ldg(H.meta + bb) : make_int4(0, 0, 0, 0);
       ncc = bb >= 0 ? __ldg(H.ncol + bb) : 0;
     };
@@ -296,17 +293,20 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
       int* ids = reinterpret_cast<int*>(st + L.ids);
       T* rq = reinterpret_cast<T*>(st + L.rows_q);
       T* rr = reinterpret_cast<T*>(st + L.rows_r);
-      // dataflow: prefetch the increment rows only if every lower-colour
-      // predecessor has already written back (one non-blocking acquire pass);
-      // otherwise the block is "late" and its consumers wait and read the rows
-      // at write-back time -- the producer never stalls the ring.
-      bool inc_rows = true;
+      // dataflow: wait (acquire) until every lower-colour predecessor has
+      // written back, then gather the increment rows -- they already hold every
+      // earlier writer's contribution.  A producer only waits on smaller
+      // tickets; the consumers never wait, so the smallest unfinished ticket
+      // always progresses (all CTAs are co-resident).
+      const bool inc_rows = true;
       if constexpr (DATAFLOW) {
         const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
-        bool done = true;
-        for (int i = lane; i < nq; i += 32) done &= ld_acquire_gpu(H.flags + __ldg(H.preds + q0 + i)) == H.epoch;
-        inc_rows = __all_sync(0xffffffffu, done);
-        if (lane == 0) hdr[8] = inc_rows ? 0 : 1;
+        for (int i = lane; i < nq; i += 32) {
+          const uint32_t* f = H.flags + __ldg(H.preds + q0 + i);
+          while (ld_acquire_gpu(f) != H.epoch) __nanosleep(64);
+        }
+        __syncwarp();
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired rows -> bulk (async-proxy) reads
       }
       constexpr bool BULK_R = LAYOUT == MP_AOS && (IC * (int)sizeof(T)) % 16 == 0;
       constexpr bool BULK_Q_T = LAYOUT == MP_AOS && RC > 0 && (RC * (int)sizeof(T)) % 16 == 0;
@@ -435,18 +435,6 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
             for (int c = 0; c < IC; ++c) sh_inc[(q * IC + c) * kp + t] = o[q][c];
         }
         named_sync(1, nc_threads);
-        bool late = false;
-        if constexpr (DATAFLOW) {
-          late = hdr[8] != 0;
-          if (late) {
-            const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
-            for (int i = t; i < nq; i += nc_threads) {
-              const uint32_t* f = H.flags + __ldg(H.preds + q0 + i);
-              while (ld_acquire_gpu(f) != H.epoch) __nanosleep(32);
-            }
-            named_sync(1, nc_threads);
-          }
-        }
         const uint16_t* po = reinterpret_cast<const uint16_t*>(st + L.poff) + hdr[13];
         const uint16_t* pr = reinterpret_cast<const uint16_t*>(st + L.pref) + hdr[14];
         for (int j = t; j < ns; j += nc_threads) {
@@ -462,7 +450,7 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
 #pragma unroll
           for (int c = 0; c < IC; ++c) {
             T* a = v.inc + ind_index<LAYOUT>(p, c, IC, v.npts);
-            *a = (late ? ld_cg(a) : rr[j * IC + c]) + acc[c];
+            *a = rr[j * IC + c] + acc[c];
           }
         }
         named_sync(1, nc_threads);
@@ -486,30 +474,18 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
       }
       if (nc == 0) named_sync(1, nc_threads);
       // write back rows + increments, re-zero the increment region
-      bool late = false;
-      if constexpr (DATAFLOW) {
-        late = hdr[8] != 0;
-        if (late) {  // the producer found a predecessor still running: wait, then read rows from L2
-          const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
-          for (int i = t; i < nq; i += nc_threads) {
-            const uint32_t* f = H.flags + __ldg(H.preds + q0 + i);
-            while (ld_acquire_gpu(f) != H.epoch) __nanosleep(32);
-          }
-          named_sync(1, nc_threads);
-        }
-      }
       if constexpr (LAYOUT == MP_AOS) {
         for (int i = t; i < ns * IC; i += nc_threads) {
           const int j = i / IC, c = i - j * IC;
           T* a = v.inc + (int64_t)ids[j] * IC + c;
-          *a = (late ? ld_cg(a) : rr[i]) + sh_inc[i];
+          *a = rr[i] + sh_inc[i];
           sh_inc[i] = T(0);
         }
       } else {
         for (int i = t; i < ns * IC; i += nc_threads) {
           const int c = i / ns, j = i - c * ns;
           T* a = v.inc + (int64_t)c * v.npts + ids[j];
-          *a = (late ? ld_cg(a) : rr[j * IC + c]) + sh_inc[j * IC + c];
+          *a = rr[j * IC + c] + sh_inc[j * IC + c];
         }
         named_sync(1, nc_threads);
         for (int i = t; i < ns * IC; i += nc_threads) sh_inc[i] = T(0);
@@ -522,13 +498,6 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
         }
         mbar_arrive(&empty[s]);
       }
-    }
-  }
-  if constexpr (DATAFLOW) {
-    __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(&H.tickets[1], 1u) == gridDim.x - 1) {
-      H.tickets[0] = 0u;  // last CTA out re-arms the counters
-      H.tickets[1] = 0u;
     }
   }
 }

@@ -32,6 +32,8 @@ SCHEDULES = {
     "pipelined-dataflow": (_native.MP_SCHED_DATAFLOW, True),
     "pipelined-pull": (_native.MP_SCHED_COLOUR | _native.MP_SCHED_PULL, True),
     "pipelined-dataflow-pull": (_native.MP_SCHED_DATAFLOW | _native.MP_SCHED_PULL, True),
+    "stream": (_native.MP_SCHED_COLOUR, "stream"),
+    "stream-dataflow": (_native.MP_SCHED_DATAFLOW, "stream"),
 }
 TORCH_DTYPES = {"f64": torch.float64, "f32": torch.float32, "i64": torch.int64, "i32": torch.int32}
 
@@ -161,7 +163,7 @@ class DeviceLoop:
     tensors: dict
     loop: _native.MpLoop
     schedule: int = _native.MP_SCHED_DATAFLOW
-    pipelined: bool = False
+    pipelined: bool | str = False  # True: warp-specialised kernel, "stream": streamed kernel
     launches: int = 0
     _keep: list = field(default_factory=list)
 
@@ -176,7 +178,8 @@ class DeviceLoop:
         else:
             if self.schedule & 3 == _native.MP_SCHED_DATAFLOW:
                 dp.epoch = dp.epoch % 0xFFFFFFFF + 1  # flags hold the last epoch; never 0
-            fn = "mp_exec_hier_pipelined" if self.pipelined else "mp_exec_hier"
+            fn = ("mp_exec_hier_stream" if self.pipelined == "stream" else
+                  "mp_exec_hier_pipelined" if self.pipelined else "mp_exec_hier")
             _native.call(fn, self.loop, dp.struct_cached(), self.schedule, max(dp.epoch, 1), sp)
 
     def run_host(self, inputs: dict, out, stream=None) -> None:
@@ -397,7 +400,7 @@ def _report(plan, kernel, loop: DeviceLoop, ms: float | None) -> MetricsReport:
         "hier", n, loop.launches_per_run(), plan.block_colours.num_colours, ub, tb, ops, occ, bps,
         reuse_factor(plan), int(plan.thread_colour_counts.max()) if nb else 0,
         float(plan.thread_colour_counts.mean()) if nb else 0.0, int(sync.sum()) if nb else 0, sync, smax, nb,
-        ("pipelined-" if loop.pipelined else "") + ("dataflow" if loop.schedule & 3 == _native.MP_SCHED_DATAFLOW
+        ("stream-" if loop.pipelined == "stream" else "pipelined-" if loop.pipelined else "") + ("dataflow" if loop.schedule & 3 == _native.MP_SCHED_DATAFLOW
                                                     else "colour") + ("-pull" if loop.schedule & 4 else ""),
         ms, gbps,
     )

@@ -302,6 +302,32 @@ class DevicePlan:
     pull_ref: torch.Tensor | None = None  # int16 local refs e*arity+s
     lag: int = DATAFLOW_LAG
     epoch: int = 0
+    tdesc_colour: torch.Tensor | None = None  # int32 [nb][4] per ticket, blocks_by_colour order
+    tdesc_order: torch.Tensor | None = None   # int32 [nb][4] per ticket, dataflow order
+    elem_meta: torch.Tensor | None = None     # uint8 [n * elem_meta_bytes] slots + colour records
+    elem_meta_bytes: int = 0
+
+    def finish_stream(self) -> None:
+        """Streamed-executor structures: ticket descriptors {e0, k | nc << 16,
+        s0, ns} in both schedule orders and packed per-element records (arity
+        local slots, thread colour byte, zero padding to a 4-byte multiple)."""
+        nb = self.block_offsets.numel() - 1
+        dev = self.meta.device
+        base = self.meta.clone()
+        if nb:
+            base[:, 1] |= self.colour_counts.to(torch.int32) << 16
+        self.tdesc_colour = base[self.blocks_by_colour.long()].contiguous() if nb else base
+        self.tdesc_order = base[self.order.long()].contiguous() if nb else base
+        n = int(self.block_offsets[-1]) if nb else 0
+        arity = self.map.shape[1]
+        sb = self.local_slots.element_size()
+        em = (arity * sb + 1 + 3) & ~3
+        rec = torch.zeros(n + 4, em, dtype=torch.uint8, device=dev)
+        if n:
+            rec[:n, : arity * sb] = self.local_slots[: n * arity].contiguous().view(torch.uint8).view(n, arity * sb)
+            rec[:n, arity * sb] = self.thread_colours[:n]
+        self.elem_meta = rec.reshape(-1)
+        self.elem_meta_bytes = em
 
     def struct(self) -> "_native.MpHierPlan":
         p = _native.MpHierPlan()
@@ -323,6 +349,12 @@ class DevicePlan:
         if self.pull_off is not None:
             p.pull_off = self.pull_off.data_ptr()
             p.pull_ref = self.pull_ref.data_ptr()
+        if self.elem_meta is None:
+            self.finish_stream()
+        p.tdesc_colour = self.tdesc_colour.data_ptr()
+        p.tdesc_order = self.tdesc_order.data_ptr()
+        p.elem_meta = self.elem_meta.data_ptr()
+        p.elem_meta_bytes = int(self.elem_meta_bytes)
         return p
 
     def reschedule(self, lag: int) -> None:
@@ -331,6 +363,7 @@ class DevicePlan:
         self.pred_off, self.preds, self.order = block_dag(self.written_off, self.written_ids, self.npts,
                                                           self.block_colours, ncol, lag)
         self.lag = lag
+        self.elem_meta = None  # ticket descriptors follow the order
         self.__dict__.pop("_struct", None)
 
 
