@@ -13,8 +13,9 @@
 //     cp.async (LDGSTS) multistage ring keeps D blocks in flight while one is
 //     computed (one commit group per block, wait_group D-1, one barrier);
 //   * the dependent chain ticket descriptor -> staged ids -> row gathers is
-//     software-pipelined in registers one block apart, so no thread waits on
-//     an index load: descriptor loads run 2 blocks ahead, id loads 1 ahead;
+//     software-pipelined in registers: an iteration's top loads the next
+//     fill's descriptor and this fill's ids, its bottom issues the gathers,
+//     so no thread waits on an index load;
 //   * gathers are issued by all lanes (32 rows per warp instruction), row by
 //     row from the block's ascending deduplicated staged list;
 //   * shared rows use an odd number of 16/8/4-byte granules as pitch
@@ -97,16 +98,33 @@ __device__ __forceinline__ int ld_acquire_cta(const int* p) {
 __device__ __forceinline__ void st_release_cta(int* p, int v) {
   asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(saddr(p)), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Row format in shared memory: access granule and a pitch holding an odd
-// number of granules (consecutive rows then hit disjoint banks).
+// Row format in shared memory.  A row of RB bytes is accessed in granules of
+// G = 16/8/4 bytes (the widest dividing RB); N = RB/G granules.  Rows are
+// packed at pitch RB when N is odd (consecutive rows then start in distinct
+// bank groups); when N is a power of two >= 2 (16-byte granules: 32-, 64-,
+// 128-byte rows) granule c of row r is stored at slot c ^ ((r / (8/N)) % N),
+// an XOR swizzle that keeps any 8 consecutive rows' granules in distinct
+// 16-byte bank groups without padding; other even N are padded by one granule.
 template <int RB>
 struct RowFmt {
   static constexpr int G = RB % 16 == 0 ? 16 : (RB % 8 == 0 ? 8 : 4);
-  static constexpr int PITCH = RB == 0 ? 0 : (((RB / G) % 2 == 1) ? RB : RB + G);
+  static constexpr int N = RB / G;
+  static constexpr bool SWZ = G == 16 && N >= 2 && N <= 8 && (N & (N - 1)) == 0;
+  static constexpr int PITCH = RB == 0 ? 0 : ((N % 2 == 1 || SWZ) ? RB : RB + G);
+  static constexpr int SHIFT = N == 2 ? 2 : (N == 4 ? 1 : 0);
+  __device__ __forceinline__ static int slot(int r, int c) {
+    if constexpr (SWZ) return r * PITCH + ((c ^ ((r >> SHIFT) & (N - 1))) * G);
+    else return r * PITCH + c * G;
+  }
 };
 
 template <int G>
@@ -118,47 +136,68 @@ struct Gran<8> { using type = uint2; };
 template <>
 struct Gran<4> { using type = uint32_t; };
 
-// shared row -> registers / registers -> shared row, granule-wide accesses
-template <typename T, int N, int G>
-__device__ __forceinline__ void lds_row(const unsigned char* p, T (&out)[N]) {
-  using V = typename Gran<G>::type;
-  constexpr int RB = N * (int)sizeof(T);
+// shared row r -> registers / registers -> shared row r (granule accesses)
+template <typename T, int NC>
+__device__ __forceinline__ void lds_row(const unsigned char* base, int r, T (&out)[NC]) {
+  using F = RowFmt<NC * (int)sizeof(T)>;
+  using V = typename Gran<F::G>::type;
 #pragma unroll
-  for (int ch = 0; ch < RB / G; ++ch) {
-    V x = *reinterpret_cast<const V*>(p + ch * G);
-    memcpy(reinterpret_cast<unsigned char*>(out) + ch * G, &x, G);
+  for (int c = 0; c < F::N; ++c) {
+    V x = *reinterpret_cast<const V*>(base + F::slot(r, c));
+    memcpy(reinterpret_cast<unsigned char*>(out) + c * F::G, &x, F::G);
   }
 }
-template <typename T, int N, int G>
-__device__ __forceinline__ void sts_row(unsigned char* p, const T (&in)[N]) {
-  using V = typename Gran<G>::type;
-  constexpr int RB = N * (int)sizeof(T);
+template <typename T, int NC>
+__device__ __forceinline__ void sts_row(unsigned char* base, int r, const T (&in)[NC]) {
+  using F = RowFmt<NC * (int)sizeof(T)>;
+  using V = typename Gran<F::G>::type;
 #pragma unroll
-  for (int ch = 0; ch < RB / G; ++ch) {
+  for (int c = 0; c < F::N; ++c) {
     V x;
-    memcpy(&x, reinterpret_cast<const unsigned char*>(in) + ch * G, G);
-    *reinterpret_cast<V*>(p + ch * G) = x;
+    memcpy(&x, reinterpret_cast<const unsigned char*>(in) + c * F::G, F::G);
+    *reinterpret_cast<V*>(base + F::slot(r, c)) = x;
   }
 }
 
-// global row (point p) of an indirect array -> shared row (async).  AoS rows
-// of `comps` components copy their first N components.
-template <typename T, int N, int LAYOUT>
-__device__ __forceinline__ void gather_row(unsigned char* dst, const T* g, int64_t p, int comps, int64_t npts) {
-  constexpr int RB = N * (int)sizeof(T);
-  constexpr int G = RowFmt<RB>::G;
+// global row (point p) of an indirect array -> shared row r (async).  AoS rows
+// of `comps` components copy their first NC components.
+template <typename T, int NC, int LAYOUT>
+__device__ __forceinline__ void gather_row(unsigned char* base, int r, const T* g, int64_t p, int comps,
+                                           int64_t npts) {
+  using F = RowFmt<NC * (int)sizeof(T)>;
   if constexpr (LAYOUT == MP_AOS) {
     const unsigned char* src = reinterpret_cast<const unsigned char*>(g + p * comps);
-    if ((comps * (int)sizeof(T)) % G == 0) {
+    if ((comps * (int)sizeof(T)) % F::G == 0) {
 #pragma unroll
-      for (int ch = 0; ch < RB / G; ++ch) cpa<G>(dst + ch * G, src + ch * G);
-    } else {
+      for (int c = 0; c < F::N; ++c) cpa<F::G>(base + F::slot(r, c), src + c * F::G);
+      return;
+    }
+  }
+  // element-wise (SoA planes, or AoS rows whose stride breaks the granule)
+  constexpr int PER = F::G / (int)sizeof(T);
 #pragma unroll
-      for (int c = 0; c < N; ++c) cpa<(int)sizeof(T)>(dst + c * sizeof(T), src + c * sizeof(T));
+  for (int c = 0; c < NC; ++c) {
+    const T* s = LAYOUT == MP_AOS ? g + p * comps + c : g + (int64_t)c * npts + p;
+    cpa<(int)sizeof(T)>(base + F::slot(r, c / PER) + (c % PER) * (int)sizeof(T), s);
+  }
+}
+
+// global row of an incremented array -> registers (L2 path when `cg`)
+template <typename T, int NC, int LAYOUT>
+__device__ __forceinline__ void ldg_row(const T* g, int64_t p, int64_t npts, bool cg, T (&out)[NC]) {
+  constexpr int RB = NC * (int)sizeof(T);
+  if constexpr (LAYOUT == MP_AOS) {
+    constexpr int G = RB % 16 == 0 ? 16 : (RB % 8 == 0 ? 8 : 4);
+    using V = typename Gran<G>::type;
+    const V* src = reinterpret_cast<const V*>(g + p * NC);
+#pragma unroll
+    for (int c = 0; c < RB / G; ++c) {
+      V x = cg ? __ldcg(src + c) : *(src + c);
+      memcpy(reinterpret_cast<unsigned char*>(out) + c * G, &x, G);
     }
   } else {
 #pragma unroll
-    for (int c = 0; c < N; ++c) cpa<(int)sizeof(T)>(dst + c * sizeof(T), g + (int64_t)c * npts + p);
+    for (int c = 0; c < NC; ++c) out[c] = cg ? __ldcg(g + (int64_t)c * npts + p) : g[(int64_t)c * npts + p];
   }
 }
 
@@ -167,14 +206,13 @@ template <class Op, typename T>
 struct StreamLayout {
   static constexpr int QB = RcArr<Op>::N * (int)sizeof(T), IB = Op::IC * (int)sizeof(T);
   static constexpr int QP = RowFmt<QB>::PITCH, IP = RowFmt<IB>::PITCH;
-  int ids, q, r, dir, em, bytes, inc, ctl, total;
+  int ids, q, dir, em, bytes, inc, ctl, total;
   __host__ __device__ static int a16(int x) { return (x + 15) & ~15; }
   __host__ __device__ StreamLayout(int ms, int mb, int em_bytes, bool stage_reads, int nstage) {
     const int qrows = Op::RC == 0 ? 0 : (stage_reads ? ms : mb * Op::ARITY);
     ids = 16;
     q = a16(ids + ms * 4);
-    r = a16(q + qrows * QP);
-    dir = a16(r + ms * IP);
+    dir = a16(q + qrows * QP);
     em = a16(dir + Op::DC * mb * (int)sizeof(T));
     bytes = a16(em + mb * em_bytes);
     inc = nstage * bytes;
@@ -183,13 +221,10 @@ struct StreamLayout {
   }
 };
 
-template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT>
-__global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, StreamView H) {
+template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR>
+__global__ void __maxnreg__(80) hier_stream_kernel(LoopView<T> v, StreamView H) {
   constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
   using L_t = StreamLayout<Op, T>;
-  constexpr int QP = L_t::QP, IP = L_t::IP;
-  constexpr int QG = RowFmt<L_t::QB>::G, IG = RowFmt<L_t::IB>::G;
-  constexpr int MAXR = A;  // staged rows per thread: ns <= A * k <= A * nt
   extern __shared__ __align__(16) unsigned char smem[];
   const int NT = H.nt, D = H.depth, NS = H.depth + 1;
   const bool stage_reads = RC > 0 && H.stage_reads != 0;
@@ -200,7 +235,7 @@ __global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, Stream
   const int G = gridDim.x;
   const int total = H.ntickets > (int)blockIdx.x ? (H.ntickets - (int)blockIdx.x + G - 1) / G : 0;
 
-  for (int i = tid; i < H.max_staged * IP / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sh_inc)[i] = 0u;
+  for (int i = tid; i < H.max_staged * L_t::IP / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sh_inc)[i] = 0u;
   if (tid == 0) {
     ctl[0] = 0;
     ctl[1] = 0;
@@ -209,40 +244,41 @@ __global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, Stream
 
   if (DATAFLOW && tid >= NT) {
     // ------------------------------ sync warp ------------------------------
+    // Relaxed polling of predecessor flags; one gpu fence per loop pass makes
+    // the observed flags acquires (before the ready count is published) and
+    // the CTA's finished write-backs releases (before their flags are set).
     const int lane = tid & 31;
     int u = 0, released = 0;
     for (;;) {
-      bool progressed = false;
       const int done = ld_acquire_cta(ctl + 0);
-      if (done > released) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the CTA's write-backs before the flags
+      int nu = u;
+      for (int scan = 0; scan < 4 && nu < total; ++scan) {  // ready fills, in order
+        const int b = __ldg(H.tblock + (int)blockIdx.x + nu * G);
+        const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
+        bool ok = true;
+        for (int i = lane; i < nq; i += 32) ok &= ld_relaxed_gpu(H.flags + __ldg(H.preds + q0 + i)) == H.epoch;
+        if (!__all_sync(0xffffffffu, ok)) break;
+        ++nu;
+      }
+      if (done > released || nu > u) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         for (int f = released + lane; f < done; f += 32)
           st_relaxed_gpu(H.flags + __ldg(H.tblock + (int)blockIdx.x + f * G), H.epoch);
         released = done;
-        progressed = true;
+        if (nu > u && lane == 0) st_release_cta(ctl + 1, nu);
+        u = nu;
+      } else {
+        __nanosleep(64);
       }
       if (released >= total) break;
-      if (u < total) {
-        const int b = __ldg(H.tblock + (int)blockIdx.x + u * G);
-        const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
-        bool ok = true;
-        for (int i = lane; i < nq; i += 32) ok &= ld_acquire_gpu(H.flags + __ldg(H.preds + q0 + i)) == H.epoch;
-        if (__all_sync(0xffffffffu, ok)) {
-          ++u;
-          if (lane == 0) st_release_cta(ctl + 1, u);
-          progressed = true;
-        }
-      }
-      if (!progressed) __nanosleep(100);
     }
     return;
   }
 
   // ------------------------------ compute threads ------------------------------
   const int t = tid;
-  auto ticket = [&](int f) { return (int)blockIdx.x + f * G; };
   auto load_desc = [&](int f) -> int4 {
-    return f < total ? __ldg(H.tdesc + ticket(f)) : make_int4(0, 0, 0, 0);
+    return f < total ? __ldg(H.tdesc + (int)blockIdx.x + f * G) : make_int4(0, 0, 0, 0);
   };
   auto load_ids = [&](const int4& d, int (&ids)[MAXR]) {
 #pragma unroll
@@ -258,14 +294,14 @@ __global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, Stream
       for (int s = 0; s < A; ++s) mp[s] = on ? map_at(v, (int64_t)d.x + t, s) : 0;
     }
   };
-  unsigned late_bits = 0;
-  auto issue_fill = [&](int f, const int4& d, const int (&ids)[MAXR], const int (&mp)[A]) {
-    const int s = f % NS;
+  uint64_t row_bits = 0;  // bit s*MAXR + r: this thread's row r of the block in stage s exists
+  auto issue_fill = [&](int s, const int4& d, const int (&ids)[MAXR], const int (&mp)[A]) {
     unsigned char* st = smem + s * L.bytes;
     const int k = d.y & 0xffff, ns = d.w;
-    bool rows_ok = true;
-    if constexpr (DATAFLOW) rows_ok = ld_acquire_cta(ctl + 1) > f;
-    late_bits = (late_bits & ~(1u << s)) | (rows_ok ? 0u : (1u << s));
+    uint64_t bits = 0;
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r) bits |= (uint64_t)(t + r * NT < ns) << r;
+    row_bits = (row_bits & ~(((uint64_t(1) << MAXR) - 1) << (s * MAXR))) | (bits << (s * MAXR));
     if (t == 0) {
       int* hdr = reinterpret_cast<int*>(st);
       hdr[0] = k;
@@ -278,8 +314,7 @@ __global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, Stream
       if (j < ns) {
         const int p = ids[r];
         reinterpret_cast<int*>(st + L.ids)[j] = p;
-        if (stage_reads) gather_row<T, RCN, LAYOUT>(st + L.q + j * QP, v.ind, p, v.ind_comps, v.npts);
-        if (rows_ok) gather_row<T, IC, LAYOUT>(st + L.r + j * IP, v.inc, p, IC, v.npts);
+        if (stage_reads) gather_row<T, RCN, LAYOUT>(st + L.q, j, v.ind, p, v.ind_comps, v.npts);
       }
     }
     if (t < k) {
@@ -298,17 +333,35 @@ __global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, Stream
       }
       if (RC > 0 && !stage_reads) {
 #pragma unroll
-        for (int sl = 0; sl < A; ++sl)
-          gather_row<T, RCN, LAYOUT>(st + L.q + (t * A + sl) * QP, v.ind, mp[sl], v.ind_comps, v.npts);
+        for (int sl = 0; sl < A; ++sl) gather_row<T, RCN, LAYOUT>(st + L.q, t * A + sl, v.ind, mp[sl], v.ind_comps, v.npts);
       }
     }
   };
-
-  // prologue: fills 0 .. D-1, then the register pipeline for fill D, D+1
-  int ids_fill[MAXR], ids_next[MAXR];
-  int map_fill[A], map_next[A];
+  // increment rows of block f (staged ids of stage s) -> registers; on the
+  // dataflow schedule only once the block's predecessors are known done
+  T rrow[MAXR][IC];
+  bool rows_late = false;
+  auto load_rows = [&](int f, int s) {
+    const unsigned char* st = smem + s * L.bytes;
+    rows_late = false;
+    if constexpr (DATAFLOW) rows_late = ld_acquire_cta(ctl + 1) <= f;
+    if (rows_late) return;
 #pragma unroll
-  for (int s = 0; s < A; ++s) map_fill[s] = map_next[s] = 0;
+    for (int r = 0; r < MAXR; ++r) {
+      const int j = t + r * NT;
+      if ((row_bits >> (s * MAXR + r)) & 1u) ldg_row<T, IC, LAYOUT>(v.inc, reinterpret_cast<const int*>(st + L.ids)[j], v.npts, DATAFLOW, rrow[r]);
+    }
+  };
+
+  // Prologue: fills 0 .. D-1 and block 0's increment rows.  Steady state,
+  // iteration i: the top loads the descriptor of fill i+D+1 and the staged
+  // ids (map rows) of fill i+D (descriptor loaded one iteration earlier); the
+  // bottom issues fill i+D and loads block i+1's increment rows.  Every
+  // register load has a whole iteration to land before its first use.
+  int ids_fill[MAXR];
+  int map_fill[A];
+#pragma unroll
+  for (int s = 0; s < A; ++s) map_fill[s] = 0;
   for (int f = 0; f < D; ++f) {
     const int4 d = load_desc(f);
     load_ids(d, ids_fill);
@@ -317,30 +370,26 @@ __global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, Stream
     cp_commit();
   }
   int4 d_fill = load_desc(D);
-  int4 d_next = load_desc(D + 1);
-  load_ids(d_fill, ids_fill);
-  load_map(d_fill, map_fill);
+  load_rows(0, 0);  // the ids are this thread's own shared stores: no wait
 
   auto cbar = [&]() {
     if constexpr (DATAFLOW) named_sync(1, NT);
     else __syncthreads();
   };
 
+  int s = 0;       // stage of block i
+  int s_fill = D;  // stage of fill i+D (= stage of block i-1)
   for (int i = 0; i < total; ++i) {
-    // a. descriptor two fills ahead, staged ids (and map rows) one fill ahead
-    const int4 d_next2 = load_desc(i + D + 2);
-    load_ids(d_next, ids_next);
-    load_map(d_next, map_next);
+    // a. loads for the bottom of this iteration and the next one
+    const int4 d_next = load_desc(i + D + 1);
+    load_ids(d_fill, ids_fill);
+    load_map(d_fill, map_fill);
     // b. block i has landed (D-1 younger groups may still be in flight)
     cp_wait(D - 1);
     cbar();
     if (DATAFLOW && t == 0) st_release_cta(ctl + 0, i);  // blocks < i are written back
-    // c. refill the stage block i-1 used
-    issue_fill(i + D, d_fill, ids_fill, map_fill);
-    cp_commit();
 
-    // d. compute block i
-    const int s = i % NS;
+    // c. compute block i
     const unsigned char* st = smem + s * L.bytes;
     const int* hdr = reinterpret_cast<const int*>(st);
     const int k = hdr[0], ns = hdr[1], nc = hdr[2];
@@ -359,29 +408,26 @@ __global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, Stream
       T r[A][RCN];
       if constexpr (RC > 0) {
 #pragma unroll
-        for (int q = 0; q < A; ++q)
-          lds_row<T, RCN, QG>(st + L.q + (stage_reads ? ls[q] : t * A + q) * QP, r[q]);
+        for (int q = 0; q < A; ++q) lds_row<T, RCN>(st + L.q, stage_reads ? ls[q] : t * A + q, r[q]);
       }
       compute<Op, T>(v, r, dd, o);
     }
-    // e. thread colours, one at a time
+    // d. thread colours, one at a time
     for (int c = 0; c < nc; ++c) {
       if (my_tc == c) {
 #pragma unroll
         for (int q = 0; q < A; ++q) {
-          unsigned char* row = sh_inc + ls[q] * IP;
           T acc[IC];
-          lds_row<T, IC, IG>(row, acc);
+          lds_row<T, IC>(sh_inc, ls[q], acc);
 #pragma unroll
           for (int cc = 0; cc < IC; ++cc) acc[cc] += o[q][cc];
-          sts_row<T, IC, IG>(row, acc);
+          sts_row<T, IC>(sh_inc, ls[q], acc);
         }
       }
       cbar();
     }
-    // f. write back: row + increment, once per staged row; re-zero the row
-    const bool late = DATAFLOW && ((late_bits >> s) & 1u);
-    if (DATAFLOW && late && t < ns) {
+    // e. write back: row + increment, once per staged row; re-zero the row
+    if (DATAFLOW && rows_late && t < ns) {
       while (ld_acquire_cta(ctl + 1) <= i) __nanosleep(32);
     }
 #pragma unroll
@@ -389,23 +435,18 @@ __global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, Stream
       const int j = t + r * NT;
       if (j < ns) {
         const int64_t p = reinterpret_cast<const int*>(st + L.ids)[j];
-        unsigned char* irow = sh_inc + j * IP;
-        T acc[IC], base[IC];
-        lds_row<T, IC, IG>(irow, acc);
-        if (late) {
+        T acc[IC];
+        lds_row<T, IC>(sh_inc, j, acc);
+        if (DATAFLOW && rows_late) ldg_row<T, IC, LAYOUT>(v.inc, p, v.npts, true, rrow[r]);
 #pragma unroll
-          for (int c = 0; c < IC; ++c) base[c] = ld_cg(v.inc + ind_index<LAYOUT>(p, c, IC, v.npts));
-        } else {
-          lds_row<T, IC, IG>(st + L.r + j * IP, base);
-        }
-#pragma unroll
-        for (int c = 0; c < IC; ++c) acc[c] = base[c] + acc[c];
+        for (int c = 0; c < IC; ++c) acc[c] = rrow[r][c] + acc[c];
         if constexpr (LAYOUT == MP_AOS) {
-          constexpr int GG = (IC * (int)sizeof(T)) % 16 == 0 ? 16 : ((IC * (int)sizeof(T)) % 8 == 0 ? 8 : 4);
+          constexpr int RB = IC * (int)sizeof(T);
+          constexpr int GG = RB % 16 == 0 ? 16 : (RB % 8 == 0 ? 8 : 4);
           using V = typename Gran<GG>::type;
           unsigned char* dst = reinterpret_cast<unsigned char*>(v.inc + p * IC);
 #pragma unroll
-          for (int ch = 0; ch < IC * (int)sizeof(T) / GG; ++ch) {
+          for (int ch = 0; ch < RB / GG; ++ch) {
             V x;
             memcpy(&x, reinterpret_cast<const unsigned char*>(acc) + ch * GG, GG);
             *reinterpret_cast<V*>(dst + ch * GG) = x;
@@ -417,16 +458,19 @@ __global__ void __launch_bounds__(1024) hier_stream_kernel(LoopView<T> v, Stream
         T z[IC];
 #pragma unroll
         for (int c = 0; c < IC; ++c) z[c] = T(0);
-        sts_row<T, IC, IG>(irow, z);
+        sts_row<T, IC>(sh_inc, j, z);
       }
     }
-    // g. rotate the register pipeline
+    // f. issue fill i+D into the stage block i-1 used (every thread passed
+    //    this iteration's barrier after finishing block i-1); load block
+    //    i+1's increment rows (its ids were stored by this thread)
+    issue_fill(s_fill, d_fill, ids_fill, map_fill);
+    cp_commit();
+    const int s_next = s + 1 == NS ? 0 : s + 1;
+    load_rows(i + 1, s_next);
     d_fill = d_next;
-    d_next = d_next2;
-#pragma unroll
-    for (int r = 0; r < MAXR; ++r) ids_fill[r] = ids_next[r];
-#pragma unroll
-    for (int q = 0; q < A; ++q) map_fill[q] = map_next[q];
+    s_fill = s;
+    s = s_next;
   }
   cp_wait(0);
   if constexpr (DATAFLOW) {
@@ -456,8 +500,13 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
     MP_FAIL(MP_ERR_CAPACITY, "streamed executor needs %zu shared bytes, over the 232448-byte limit", smem);
   H.depth = depth;
   const int threads = nt + (dataflow ? 32 : 0);
-  if (threads > 1024) MP_FAIL(MP_ERR_CAPACITY, "block size %d exceeds the CTA thread limit", P.block_size);
-  auto kern = dataflow ? hier_stream_kernel<Op, T, LAYOUT, true, SlotT> : hier_stream_kernel<Op, T, LAYOUT, false, SlotT>;
+  if (threads > 512) MP_FAIL(MP_ERR_CAPACITY, "block size %d exceeds the streamed executor limit of 480", P.block_size);
+  // staged rows per thread (ns <= ARITY * k): 2 for pair loops, 4 or 8 otherwise
+  constexpr int R_LO = Op::ARITY <= 2 ? 2 : 4, R_HI = Op::ARITY <= 2 ? 2 : 8;
+  const bool hi = P.max_staged > R_LO * nt;
+  if (P.max_staged > R_HI * nt) MP_FAIL(MP_ERR_CAPACITY, "block stages %d rows, over %d per CTA", P.max_staged, R_HI * nt);
+  auto kern = dataflow ? (hi ? hier_stream_kernel<Op, T, LAYOUT, true, SlotT, R_HI> : hier_stream_kernel<Op, T, LAYOUT, true, SlotT, R_LO>)
+                       : (hi ? hier_stream_kernel<Op, T, LAYOUT, false, SlotT, R_HI> : hier_stream_kernel<Op, T, LAYOUT, false, SlotT, R_LO>);
   MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, dev = 0, sms = 0;
   MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
