@@ -41,8 +41,10 @@ CONFIGS = {
     "C5": ("quad2d", (5657, 5657), "flux", "f64", "all-indirect"),
 }
 METRIC = "effective HBM GB/s and ms/iter per indirect loop vs global colouring, 1/2/4/8 GPU"
-SCHEDULES = ("pipelined-pull", "pipelined", "colour", "pipelined-dataflow-pull", "pipelined-dataflow", "dataflow")
+SCHEDULES = ("stream", "stream-dataflow", "pipelined", "pipelined-pull", "colour", "dataflow")
 L2_BYTES = 126 * 2**20
+KERNEL_OF = {"stream": "hier_stream_kernel", "pipelined": "hier_pipe_kernel", "colour": "hier_block_kernel",
+             "dataflow": "hier_block_kernel"}
 
 
 def peaks():
@@ -362,7 +364,7 @@ def our_arm(args):
         },
         "roofline": {"bound": "hbm", "achieved": round(gbps, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(gbps / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": f"{'hier_pipe_kernel' if 'pipelined' in args.schedule else 'hier_block_kernel'} "
+                     "kernel": f"{KERNEL_OF[args.schedule.split('-')[0]]} "
                                f"({args.schedule} schedule, {launches} launch(es)/step; achieved = useful "
                                f"bytes / summed device time of the step's launches)"},
         "e2e": {"value": round(ub / (statistics.median(e2e_times) * 1e-3) / 1e9, 3), "unit": "GB/s",
@@ -389,7 +391,7 @@ def main():
     ap.add_argument("--global-reorder", default="gps")
     ap.add_argument("--layout", default="aos")
     ap.add_argument("--block-size", type=int, default=128)
-    ap.add_argument("--schedule", default="pipelined", choices=SCHEDULES)
+    ap.add_argument("--schedule", default="stream", choices=SCHEDULES)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -119,6 +119,10 @@ typedef struct mp_hier_plan {
   const uint8_t* elem_meta;       /* [n_elems*elem_meta_bytes]               */
   int32_t elem_meta_bytes;
   int32_t pad2_;
+  /* predecessor lists re-indexed by dataflow ticket: the preds (block ids)
+   * of block order[t] are tpreds[tpred_offsets[t] .. tpred_offsets[t+1]) */
+  const int32_t* tpred_offsets;   /* [nb+1]                                  */
+  const int32_t* tpreds;
 } mp_hier_plan;
 
 /* ---- library ------------------------------------------------------------ */

@@ -66,6 +66,7 @@ struct StreamView {
   int32_t nt;     // compute threads (multiple of 32)
   int32_t depth;  // blocks in flight; stages = depth + 1
   int32_t stage_reads;
+  uint32_t* stats;  // optional (MESHPLAN_STREAM_STATS): [0] late blocks
 };
 
 __device__ __forceinline__ unsigned saddr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -120,7 +121,7 @@ struct RowFmt {
   static constexpr int N = RB / G;
   static constexpr bool SWZ = G == 16 && N >= 2 && N <= 8 && (N & (N - 1)) == 0;
   static constexpr int PITCH = RB == 0 ? 0 : ((N % 2 == 1 || SWZ) ? RB : RB + G);
-  static constexpr int SHIFT = N == 2 ? 2 : (N == 4 ? 1 : 0);
+  static constexpr int SHIFT = SWZ ? (N == 2 ? 2 : (N == 4 ? 1 : 0)) : 0;
   __device__ __forceinline__ static int slot(int r, int c) {
     if constexpr (SWZ) return r * PITCH + ((c ^ ((r >> SHIFT) & (N - 1))) * G);
     else return r * PITCH + c * G;
@@ -201,6 +202,10 @@ __device__ __forceinline__ void ldg_row(const T* g, int64_t p, int64_t npts, boo
   }
 }
 
+// Control block: int counters [0] done fills, [1] ready fills (dataflow).
+constexpr int CTL_RING = 8;
+constexpr int CTL_BYTES = CTL_RING * 4;
+
 // Stage layout (bytes), identical on host and device.
 template <class Op, typename T>
 struct StreamLayout {
@@ -217,12 +222,12 @@ struct StreamLayout {
     bytes = a16(em + mb * em_bytes);
     inc = nstage * bytes;
     ctl = a16(inc + ms * IP);
-    total = ctl + 16;
+    total = ctl + CTL_BYTES;
   }
 };
 
 template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR>
-__global__ void __maxnreg__(80) hier_stream_kernel(LoopView<T> v, StreamView H) {
+__global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v, StreamView H) {
   constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
   using L_t = StreamLayout<Op, T>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -233,37 +238,45 @@ __global__ void __maxnreg__(80) hier_stream_kernel(LoopView<T> v, StreamView H) 
   int* ctl = reinterpret_cast<int*>(smem + L.ctl);  // [0] done count, [1] ready count
   const int tid = threadIdx.x;
   const int G = gridDim.x;
+  // static claims: fill f of CTA c takes ticket c + f * grid
   const int total = H.ntickets > (int)blockIdx.x ? (H.ntickets - (int)blockIdx.x + G - 1) / G : 0;
 
   for (int i = tid; i < H.max_staged * L_t::IP / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sh_inc)[i] = 0u;
-  if (tid == 0) {
-    ctl[0] = 0;
-    ctl[1] = 0;
-  }
+  if (tid < CTL_RING) ctl[tid] = 0;
   __syncthreads();
+
+  // Programmatic dependent launch: let the next launch on the stream start
+  // its CTAs (prologue gathers of read-only data) as this grid's CTAs retire;
+  // griddepcontrol.wait below guards every access to the incremented array.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (DATAFLOW && tid >= NT) {
     // ------------------------------ sync warp ------------------------------
-    // Relaxed polling of predecessor flags; one gpu fence per loop pass makes
-    // the observed flags acquires (before the ready count is published) and
-    // the CTA's finished write-backs releases (before their flags are set).
-    const int lane = tid & 31;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // Relaxed polling of predecessor flags, 8 fills x 4 predecessor slots per
+    // pass (lane = 4 * fill offset + slot; predecessor lists in ticket
+    // order); one gpu fence per pass makes the observed flags acquires (before
+    // the ready count is published) and the CTA's finished write-backs
+    // releases (before their flags are set).
+    const int lane = tid & 31, fo = lane >> 2, slot = lane & 3;
     int u = 0, released = 0;
     for (;;) {
       const int done = ld_acquire_cta(ctl + 0);
-      int nu = u;
-      for (int scan = 0; scan < 4 && nu < total; ++scan) {  // ready fills, in order
-        const int b = __ldg(H.tblock + (int)blockIdx.x + nu * G);
-        const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
-        bool ok = true;
-        for (int i = lane; i < nq; i += 32) ok &= ld_relaxed_gpu(H.flags + __ldg(H.preds + q0 + i)) == H.epoch;
-        if (!__all_sync(0xffffffffu, ok)) break;
-        ++nu;
+      const int f = u + fo;
+      bool ok = true;
+      if (f < total) {
+        const int tk = (int)blockIdx.x + f * G;
+        const int q1 = __ldg(H.pred_offsets + tk + 1);
+        for (int q = __ldg(H.pred_offsets + tk) + slot; q < q1; q += 4)
+          ok &= ld_relaxed_gpu(H.flags + __ldg(H.preds + q)) == H.epoch;
       }
+      const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+      int nu = u + (bad ? (__ffs(bad) - 1) / 4 : 8);
+      nu = nu < total ? nu : total;
       if (done > released || nu > u) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        for (int f = released + lane; f < done; f += 32)
-          st_relaxed_gpu(H.flags + __ldg(H.tblock + (int)blockIdx.x + f * G), H.epoch);
+        for (int g = released + lane; g < done; g += 32)
+          st_relaxed_gpu(H.flags + __ldg(H.tblock + (int)blockIdx.x + g * G), H.epoch);
         released = done;
         if (nu > u && lane == 0) st_release_cta(ctl + 1, nu);
         u = nu;
@@ -282,9 +295,9 @@ __global__ void __maxnreg__(80) hier_stream_kernel(LoopView<T> v, StreamView H) 
   };
   auto load_ids = [&](const int4& d, int (&ids)[MAXR]) {
 #pragma unroll
-    for (int r = 0; r < MAXR; ++r) {
+    for (int r = 0; r < MAXR; ++r) {  // unpredicated (clamped) loads: no merge copies
       const int j = t + r * NT;
-      ids[r] = j < d.w ? __ldg(H.staged_ids + d.z + j) : 0;
+      ids[r] = __ldg(H.staged_ids + max(d.z + min(j, d.w - 1), 0));
     }
   };
   auto load_map = [&](const int4& d, int (&mp)[A]) {
@@ -345,11 +358,13 @@ __global__ void __maxnreg__(80) hier_stream_kernel(LoopView<T> v, StreamView H) 
     const unsigned char* st = smem + s * L.bytes;
     rows_late = false;
     if constexpr (DATAFLOW) rows_late = ld_acquire_cta(ctl + 1) <= f;
-    if (rows_late) return;
+    // unpredicated loads (absent rows read point 0; a late block's rows are
+    // re-read after its wait), so the values land straight in rrow
 #pragma unroll
     for (int r = 0; r < MAXR; ++r) {
       const int j = t + r * NT;
-      if ((row_bits >> (s * MAXR + r)) & 1u) ldg_row<T, IC, LAYOUT>(v.inc, reinterpret_cast<const int*>(st + L.ids)[j], v.npts, DATAFLOW, rrow[r]);
+      const int p = ((row_bits >> (s * MAXR + r)) & 1u) ? reinterpret_cast<const int*>(st + L.ids)[j] : 0;
+      ldg_row<T, IC, LAYOUT>(v.inc, p, v.npts, DATAFLOW, rrow[r]);
     }
   };
 
@@ -370,6 +385,7 @@ __global__ void __maxnreg__(80) hier_stream_kernel(LoopView<T> v, StreamView H) 
     cp_commit();
   }
   int4 d_fill = load_desc(D);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous launch's increments are visible
   load_rows(0, 0);  // the ids are this thread's own shared stores: no wait
 
   auto cbar = [&]() {
@@ -388,10 +404,10 @@ __global__ void __maxnreg__(80) hier_stream_kernel(LoopView<T> v, StreamView H) 
     cp_wait(D - 1);
     cbar();
     if (DATAFLOW && t == 0) st_release_cta(ctl + 0, i);  // blocks < i are written back
-
-    // c. compute block i
     const unsigned char* st = smem + s * L.bytes;
     const int* hdr = reinterpret_cast<const int*>(st);
+
+    // c. compute block i
     const int k = hdr[0], ns = hdr[1], nc = hdr[2];
     T o[A][IC];
     int ls[A];
@@ -428,6 +444,7 @@ __global__ void __maxnreg__(80) hier_stream_kernel(LoopView<T> v, StreamView H) 
     }
     // e. write back: row + increment, once per staged row; re-zero the row
     if (DATAFLOW && rows_late && t < ns) {
+      if (H.stats && t == 0) atomicAdd(H.stats, 1u);
       while (ld_acquire_cta(ctl + 1) <= i) __nanosleep(32);
     }
 #pragma unroll
@@ -479,6 +496,24 @@ __global__ void __maxnreg__(80) hier_stream_kernel(LoopView<T> v, StreamView H) 
   }
 }
 
+// Launch with programmatic stream serialization (PDL): consecutive colour
+// launches overlap one grid's tail with the next grid's prologue.
+template <typename K, typename... Args>
+cudaError_t launch_pdl(K kern, int grid, int threads, size_t smem, cudaStream_t st, Args... args) {
+  static const bool off = getenv("MESHPLAN_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <class Op, typename T, int LAYOUT, typename SlotT>
 mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
   static const int env_depth = getenv("MESHPLAN_STREAM_DEPTH") ? atoi(getenv("MESHPLAN_STREAM_DEPTH")) : 2;
@@ -489,6 +524,17 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   H.max_block = P.block_size;
   H.max_staged = P.max_staged;
   H.stage_reads = P.stage_reads;
+  static uint32_t* stats = nullptr;
+  if (getenv("MESHPLAN_STREAM_STATS") && !stats) {
+    MP_CUDA_TRY(cudaMallocManaged(&stats, 64));
+    memset(stats, 0, 64);
+  }
+  if (stats && dataflow) {
+    MP_CUDA_TRY(cudaStreamSynchronize(st));
+    if (stats[1]++ > 0) fprintf(stderr, "[stream stats] late blocks last run: %u\n", stats[0]);
+    stats[0] = 0;
+  }
+  H.stats = stats;
   const bool sr = Op::RC > 0 && P.stage_reads;
   size_t smem = 0;
   for (;; --depth) {  // shrink the ring if it does not fit
@@ -518,10 +564,11 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   if (dataflow) {
     H.tdesc = reinterpret_cast<const int4*>(P.tdesc_order);
     H.tblock = P.order;
+    H.pred_offsets = P.tpred_offsets;  // ticket-ordered predecessor CSR
+    H.preds = P.tpreds;
     H.ntickets = P.num_blocks;
     const int grid = P.num_blocks < resident ? P.num_blocks : resident;
-    kern<<<grid, threads, smem, st>>>(v, H);
-    MP_CHECK_LAUNCH();
+    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H));
     return MP_OK;
   }
   for (int c = 0; c < P.num_block_colours; ++c) {
@@ -531,8 +578,7 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
     H.tblock = P.blocks_by_colour + lo;
     H.ntickets = hi - lo;
     const int grid = (hi - lo) < resident ? (hi - lo) : resident;
-    kern<<<grid, threads, smem, st>>>(v, H);
-    MP_CHECK_LAUNCH();
+    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H));
   }
   return MP_OK;
 }
@@ -551,7 +597,7 @@ mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool datafl
     if (P.elem_meta_bytes < Op::ARITY * P.slot_bytes + 1 || P.elem_meta_bytes % 4)
       MP_FAIL(MP_ERR_KERNEL, "element records of %d bytes cannot hold %d slots and a colour", P.elem_meta_bytes,
               Op::ARITY);
-    if (dataflow && (!P.order || !P.pred_offsets || !P.flags))
+    if (dataflow && (!P.order || !P.tpred_offsets || !P.tpreds || !P.flags))
       MP_FAIL(MP_ERR_KERNEL, "dataflow schedule needs order/preds/flags");
     StreamView H{};
     H.staged_ids = P.staged_ids;

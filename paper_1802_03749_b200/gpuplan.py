@@ -306,6 +306,8 @@ class DevicePlan:
     tdesc_order: torch.Tensor | None = None   # int32 [nb][4] per ticket, dataflow order
     elem_meta: torch.Tensor | None = None     # uint8 [n * elem_meta_bytes] slots + colour records
     elem_meta_bytes: int = 0
+    tpred_off: torch.Tensor | None = None     # int32 [nb+1] predecessor CSR in ticket order
+    tpreds: torch.Tensor | None = None        # int32 block ids
 
     def finish_stream(self) -> None:
         """Streamed-executor structures: ticket descriptors {e0, k | nc << 16,
@@ -318,6 +320,21 @@ class DevicePlan:
             base[:, 1] |= self.colour_counts.to(torch.int32) << 16
         self.tdesc_colour = base[self.blocks_by_colour.long()].contiguous() if nb else base
         self.tdesc_order = base[self.order.long()].contiguous() if nb else base
+        # predecessor lists in ticket order (one indirection less for the sync warp)
+        po = self.pred_off.long()
+        cnt = (po[1:] - po[:-1])[self.order.long()] if nb else po[:0]
+        toff = torch.zeros(nb + 1, dtype=torch.long, device=dev)
+        if nb:
+            toff[1:] = torch.cumsum(cnt, 0)
+        total = int(toff[-1]) if nb else 0
+        if total:
+            src_start = po[:-1][self.order.long()]
+            rel = torch.arange(total, device=dev) - torch.repeat_interleave(toff[:-1], cnt)
+            idx = torch.repeat_interleave(src_start, cnt) + rel
+            self.tpreds = torch.cat([self.preds.long()[idx].to(torch.int32), torch.zeros(1, dtype=torch.int32, device=dev)])
+        else:
+            self.tpreds = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.tpred_off = toff.to(torch.int32)
         n = int(self.block_offsets[-1]) if nb else 0
         arity = self.map.shape[1]
         sb = self.local_slots.element_size()
@@ -355,6 +372,8 @@ class DevicePlan:
         p.tdesc_order = self.tdesc_order.data_ptr()
         p.elem_meta = self.elem_meta.data_ptr()
         p.elem_meta_bytes = int(self.elem_meta_bytes)
+        p.tpred_offsets = self.tpred_off.data_ptr()
+        p.tpreds = self.tpreds.data_ptr()
         return p
 
     def reschedule(self, lag: int) -> None:

@@ -41,6 +41,13 @@ def raw(report: str):
     return [(dict(zip(hdr, r)), dict(zip(hdr, units))) for r in rows[2:]]
 
 
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def to_bytes(value: str, unit: str) -> float:
+    return float((value or "0").replace(",", "")) * SCALE.get(unit.strip(), 1)
+
+
 def summarise(report: str) -> str:
     data = raw(report)
     if not data:
@@ -52,9 +59,9 @@ def summarise(report: str) -> str:
         for key, label in METRICS:
             if key in vals:
                 lines.append(f"| {label} (`{key}`) | {vals[key]} {units.get(key, '')} |")
-        rd = float(vals.get("dram__bytes_read.sum", "0") or 0)
-        wr = float(vals.get("dram__bytes_write.sum", "0") or 0)
-        lines.append(f"\ntraffic (read+write): {rd + wr:.4g} {units.get('dram__bytes_read.sum', '')}\n")
+        rd = to_bytes(vals.get("dram__bytes_read.sum", "0"), units.get("dram__bytes_read.sum", "byte"))
+        wr = to_bytes(vals.get("dram__bytes_write.sum", "0"), units.get("dram__bytes_write.sum", "byte"))
+        lines.append(f"\ntraffic (read+write): {rd + wr:.6g} bytes = {(rd + wr) / 1e9:.4f} GB\n")
     return "\n".join(lines) + "\n"
 
 
