@@ -123,6 +123,9 @@ typedef struct mp_hier_plan {
    * of block order[t] are tpreds[tpred_offsets[t] .. tpred_offsets[t+1]) */
   const int32_t* tpred_offsets;   /* [nb+1]                                  */
   const int32_t* tpreds;
+  /* the same lists padded to 8 per ticket: -1 = no predecessor, -2 in slot 7 =
+   * the list continues in tpreds (from its 8th entry) */
+  const int32_t* tpred_pad;       /* [nb][8]                                 */
 } mp_hier_plan;
 
 /* ---- library ------------------------------------------------------------ */

@@ -57,6 +57,7 @@ struct StreamView {
   const unsigned char* __restrict__ emeta;  // per element: A slots, colour byte, pad
   const int32_t* __restrict__ pred_offsets;
   const int32_t* __restrict__ preds;
+  const int32_t* __restrict__ pred_pad;  // [ntickets][8] (dataflow)
   uint32_t* flags;
   uint32_t epoch;
   int32_t ntickets;
@@ -98,6 +99,9 @@ __device__ __forceinline__ int ld_acquire_cta(const int* p) {
 }
 __device__ __forceinline__ void st_release_cta(int* p, int v) {
   asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(saddr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_cta_add(int* p, int v) {
+  asm volatile("red.release.cta.shared::cta.add.s32 [%0], %1;" ::"r"(saddr(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   uint32_t v;
@@ -253,25 +257,33 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
   if (DATAFLOW && tid >= NT) {
     // ------------------------------ sync warp ------------------------------
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    // Relaxed polling of predecessor flags, 8 fills x 4 predecessor slots per
-    // pass (lane = 4 * fill offset + slot; predecessor lists in ticket
-    // order); one gpu fence per pass makes the observed flags acquires (before
+    // Readiness: lanes = 4 fills x 8 predecessor slots; the predecessor ids of
+    // the window [u, u+4) come from the ticket-ordered padded lists (-1 = none,
+    // -2 in slot 7 = more in the CSR) and stay in registers while the window
+    // waits, so a pass costs one round trip of relaxed flag loads.  One gpu
+    // fence per productive pass turns the observed flags into acquires (before
     // the ready count is published) and the CTA's finished write-backs
-    // releases (before their flags are set).
-    const int lane = tid & 31, fo = lane >> 2, slot = lane & 3;
-    int u = 0, released = 0;
+    // (counted per warp in shared memory) into releases (before their flags).
+    const int lane = tid & 31, fo = lane >> 3, slot = lane & 7;
+    const int nw = NT >> 5;
+    int u = 0, released = 0, win = -1;
+    int pid = -1;
     for (;;) {
-      const int done = ld_acquire_cta(ctl + 0);
-      const int f = u + fo;
-      bool ok = true;
-      if (f < total) {
-        const int tk = (int)blockIdx.x + f * G;
+      if (win != u) {  // (re)load the window's predecessor ids
+        const int f = u + fo;
+        pid = f < total ? __ldg(H.pred_pad + (int64_t)((int)blockIdx.x + f * G) * 8 + slot) : -1;
+        win = u;
+      }
+      bool ok = pid < 0 || ld_relaxed_gpu(H.flags + pid) == H.epoch;
+      if (pid == -2) {  // overflow: the block's 8th and later predecessors from the CSR
+        const int tk = (int)blockIdx.x + (u + fo) * G;
         const int q1 = __ldg(H.pred_offsets + tk + 1);
-        for (int q = __ldg(H.pred_offsets + tk) + slot; q < q1; q += 4)
+        for (int q = __ldg(H.pred_offsets + tk) + 7; q < q1; ++q)
           ok &= ld_relaxed_gpu(H.flags + __ldg(H.preds + q)) == H.epoch;
       }
+      const int done = ld_acquire_cta(ctl + 0) / nw;
       const unsigned bad = __ballot_sync(0xffffffffu, !ok);
-      int nu = u + (bad ? (__ffs(bad) - 1) / 4 : 8);
+      int nu = u + (bad ? (__ffs(bad) - 1) / 8 : 4);
       nu = nu < total ? nu : total;
       if (done > released || nu > u) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -281,7 +293,7 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
         if (nu > u && lane == 0) st_release_cta(ctl + 1, nu);
         u = nu;
       } else {
-        __nanosleep(64);
+        __nanosleep(32);
       }
       if (released >= total) break;
     }
@@ -403,7 +415,6 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
     // b. block i has landed (D-1 younger groups may still be in flight)
     cp_wait(D - 1);
     cbar();
-    if (DATAFLOW && t == 0) st_release_cta(ctl + 0, i);  // blocks < i are written back
     const unsigned char* st = smem + s * L.bytes;
     const int* hdr = reinterpret_cast<const int*>(st);
 
@@ -478,6 +489,10 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
         sts_row<T, IC>(sh_inc, j, z);
       }
     }
+    if constexpr (DATAFLOW) {  // this warp's write-back stores are done (release, CTA scope)
+      __syncwarp();
+      if ((t & 31) == 0) red_release_cta_add(ctl + 0, 1);
+    }
     // f. issue fill i+D into the stage block i-1 used (every thread passed
     //    this iteration's barrier after finishing block i-1); load block
     //    i+1's increment rows (its ids were stored by this thread)
@@ -490,10 +505,6 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
     s = s_next;
   }
   cp_wait(0);
-  if constexpr (DATAFLOW) {
-    named_sync(1, NT);
-    if (t == 0) st_release_cta(ctl + 0, total);
-  }
 }
 
 // Launch with programmatic stream serialization (PDL): consecutive colour
@@ -566,6 +577,7 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
     H.tblock = P.order;
     H.pred_offsets = P.tpred_offsets;  // ticket-ordered predecessor CSR
     H.preds = P.tpreds;
+    H.pred_pad = P.tpred_pad;
     H.ntickets = P.num_blocks;
     const int grid = P.num_blocks < resident ? P.num_blocks : resident;
     MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H));
@@ -597,7 +609,7 @@ mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool datafl
     if (P.elem_meta_bytes < Op::ARITY * P.slot_bytes + 1 || P.elem_meta_bytes % 4)
       MP_FAIL(MP_ERR_KERNEL, "element records of %d bytes cannot hold %d slots and a colour", P.elem_meta_bytes,
               Op::ARITY);
-    if (dataflow && (!P.order || !P.tpred_offsets || !P.tpreds || !P.flags))
+    if (dataflow && (!P.order || !P.tpred_offsets || !P.tpreds || !P.tpred_pad || !P.flags))
       MP_FAIL(MP_ERR_KERNEL, "dataflow schedule needs order/preds/flags");
     StreamView H{};
     H.staged_ids = P.staged_ids;

@@ -308,6 +308,7 @@ class DevicePlan:
     elem_meta_bytes: int = 0
     tpred_off: torch.Tensor | None = None     # int32 [nb+1] predecessor CSR in ticket order
     tpreds: torch.Tensor | None = None        # int32 block ids
+    tpred_pad: torch.Tensor | None = None     # int32 [nb][8] padded predecessor ids
 
     def finish_stream(self) -> None:
         """Streamed-executor structures: ticket descriptors {e0, k | nc << 16,
@@ -335,6 +336,14 @@ class DevicePlan:
         else:
             self.tpreds = torch.zeros(1, dtype=torch.int32, device=dev)
         self.tpred_off = toff.to(torch.int32)
+        pad = torch.full((max(nb, 1), 8), -1, dtype=torch.int32, device=dev)
+        if total:
+            slot = torch.arange(total, device=dev) - torch.repeat_interleave(toff[:-1], cnt)
+            owner = torch.repeat_interleave(torch.arange(nb, device=dev), cnt)
+            keep = slot < 8
+            pad[owner[keep], slot[keep]] = self.tpreds[:total][keep]
+            pad[cnt > 8, 7] = -2
+        self.tpred_pad = pad.reshape(-1).contiguous()
         n = int(self.block_offsets[-1]) if nb else 0
         arity = self.map.shape[1]
         sb = self.local_slots.element_size()
@@ -374,6 +383,7 @@ class DevicePlan:
         p.elem_meta_bytes = int(self.elem_meta_bytes)
         p.tpred_offsets = self.tpred_off.data_ptr()
         p.tpreds = self.tpreds.data_ptr()
+        p.tpred_pad = self.tpred_pad.data_ptr()
         return p
 
     def reschedule(self, lag: int) -> None:
