@@ -42,7 +42,10 @@
 // finished all its earlier ones, and sync warps keep releasing finished
 // blocks while they poll, so that ticket always progresses while every CTA
 // is resident (the grid is capped at the occupancy-derived resident count).
+#include <cuda.h>
 #include <stdlib.h>
+
+#include <type_traits>
 #include <string.h>
 
 #include "mp_loop.cuh"
@@ -110,6 +113,31 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---- mbarrier / TMA gather4 (staged read rows through the tensor engine) ----
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
+          saddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// four rows (r0..r3) of a 2D tensor map, {comps x 1} box each, into 4
+// consecutive shared rows (the map's swizzle applies), completing on `bar`
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(saddr(bar))
+      : "memory");
 }
 
 // Row format in shared memory.  A row of RB bytes is accessed in granules of
@@ -206,9 +234,11 @@ __device__ __forceinline__ void ldg_row(const T* g, int64_t p, int64_t npts, boo
   }
 }
 
-// Control block: int counters [0] done fills, [1] ready fills (dataflow).
+// Control block: int counters [0] done fills, [1] ready fills (dataflow),
+// then one "rows landed" mbarrier per stage (TMA path).
 constexpr int CTL_RING = 8;
-constexpr int CTL_BYTES = CTL_RING * 4;
+constexpr int MAX_NS = 6;
+constexpr int CTL_BYTES = CTL_RING * 4 + MAX_NS * 8;
 
 // Stage layout (bytes), identical on host and device.
 template <class Op, typename T>
@@ -220,21 +250,23 @@ struct StreamLayout {
   __host__ __device__ StreamLayout(int ms, int mb, int em_bytes, bool stage_reads, int nstage) {
     const int qrows = Op::RC == 0 ? 0 : (stage_reads ? ms : mb * Op::ARITY);
     ids = 16;
-    q = a16(ids + ms * 4);
-    dir = a16(q + qrows * QP);
+    q = (ids + ms * 4 + 1023) & ~1023;  // swizzle atoms (TMA) need 1024-B alignment
+    dir = a16(q + ((qrows + 3) & ~3) * QP);
     em = a16(dir + Op::DC * mb * (int)sizeof(T));
     bytes = a16(em + mb * em_bytes);
+    bytes = (bytes + 1023) & ~1023;
     inc = nstage * bytes;
     ctl = a16(inc + ms * IP);
     total = ctl + CTL_BYTES;
   }
 };
 
-template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR>
-__global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v, StreamView H) {
+template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR, bool TMAQ>
+__global__ void __maxnreg__(DATAFLOW ? 64 : 72)
+    hier_stream_kernel(LoopView<T> v, StreamView H, const __grid_constant__ CUtensorMap qmap) {
   constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
   using L_t = StreamLayout<Op, T>;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem[];
   const int NT = H.nt, D = H.depth, NS = H.depth + 1;
   const bool stage_reads = RC > 0 && H.stage_reads != 0;
   const L_t L(H.max_staged, H.max_block, H.em_bytes, stage_reads, NS);
@@ -247,6 +279,11 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
 
   for (int i = tid; i < H.max_staged * L_t::IP / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sh_inc)[i] = 0u;
   if (tid < CTL_RING) ctl[tid] = 0;
+  uint64_t* qbar = reinterpret_cast<uint64_t*>(ctl + CTL_RING);  // [NS] staged read rows landed
+  if (TMAQ && tid == 0) {
+    for (int b = 0; b < NS; ++b) mbar_init(qbar + b, NT >> 5);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
 
   // Programmatic dependent launch: let the next launch on the stream start
@@ -339,7 +376,33 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
       if (j < ns) {
         const int p = ids[r];
         reinterpret_cast<int*>(st + L.ids)[j] = p;
-        if (stage_reads) gather_row<T, RCN, LAYOUT>(st + L.q, j, v.ind, p, v.ind_comps, v.npts);
+        if (!TMAQ && stage_reads) gather_row<T, RCN, LAYOUT>(st + L.q, j, v.ind, p, v.ind_comps, v.npts);
+      }
+    }
+    if constexpr (TMAQ) {
+      // each warp gathers its own rows, four per lane-quad leader; rows past
+      // ns repeat the warp's last valid id (the q area holds ns rounded up to
+      // 4 rows).  The transaction bytes are announced before any copy issues.
+      const int lane = t & 31;
+      unsigned groups = 0;
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        const int nrow = ns - ((t & ~31) + r * NT);
+        groups += nrow <= 0 ? 0u : (unsigned)((nrow > 32 ? 32 : nrow) + 3) / 4;
+      }
+      if (lane == 0) mbar_arrive_expect(qbar + s, groups * 4u * (unsigned)L_t::QB);
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the stage before async writes
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        const int base = (t & ~31) + r * NT;
+        const int last = ns - 1 - base;  // lane holding the block's last id, if in this warp
+        const int pl = __shfl_sync(0xffffffffu, ids[r], last < 0 ? 0 : (last > 31 ? 31 : last));
+        const int pp = (base + lane) < ns ? ids[r] : pl;
+        const int p1 = __shfl_down_sync(0xffffffffu, pp, 1), p2 = __shfl_down_sync(0xffffffffu, pp, 2),
+                  p3 = __shfl_down_sync(0xffffffffu, pp, 3);
+        if ((lane & 3) == 0 && base + lane < ns)
+          tma_gather4(st + L.q + (base + lane) * L_t::QP, &qmap, pp, p1, p2, p3, qbar + s);
       }
     }
     if (t < k) {
@@ -407,6 +470,7 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
 
   int s = 0;       // stage of block i
   int s_fill = D;  // stage of fill i+D (= stage of block i-1)
+  unsigned qphase = 0;  // TMA path: expected parity of each stage's mbarrier
   for (int i = 0; i < total; ++i) {
     // a. loads for the bottom of this iteration and the next one
     const int4 d_next = load_desc(i + D + 1);
@@ -414,6 +478,10 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
     load_map(d_fill, map_fill);
     // b. block i has landed (D-1 younger groups may still be in flight)
     cp_wait(D - 1);
+    if constexpr (TMAQ) {
+      mbar_wait(qbar + s, (qphase >> s) & 1u);
+      qphase ^= 1u << s;
+    }
     cbar();
     const unsigned char* st = smem + s * L.bytes;
     const int* hdr = reinterpret_cast<const int*>(st);
@@ -507,6 +575,45 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72) hier_stream_kernel(LoopView<T> v
   cp_wait(0);
 }
 
+// ---- host: 2D row tensor maps for TMA gather4 ----
+template <typename T> constexpr int dtype_code() {
+  return std::is_same<T, double>::value ? (int)CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+       : std::is_same<T, float>::value  ? (int)CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+       : sizeof(T) == 8                 ? (int)CU_TENSOR_MAP_DATA_TYPE_INT64
+                                        : (int)CU_TENSOR_MAP_DATA_TYPE_INT32;
+}
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+#define MP_CUDA_TRY_DRV(expr)                                              \
+  do {                                                                     \
+    int _r = (expr);                                                       \
+    if (_r != 0) MP_FAIL(MP_ERR_CUDA, "tensor map encode failed (%d)", _r); \
+  } while (0)
+// rows of `comps` elements (stride comps*esize bytes), boxes of `used`
+// elements x 1 row, swizzle matching RowFmt (32/64/128-byte rows)
+inline int encode_row_map(CUtensorMap* map, const void* base, int esize, int dtype, int comps, int64_t rows,
+                          int used) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p) return -1;
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  const int rb = used * esize;
+  const CUtensorMapSwizzle sw = rb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                               : rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                               : rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                           : CU_TENSOR_MAP_SWIZZLE_NONE;
+  cuuint64_t dims[2] = {(cuuint64_t)comps, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)comps * esize};
+  cuuint32_t box[2] = {(cuuint32_t)used, 1};
+  cuuint32_t estr[2] = {1, 1};
+  return (int)fn(map, (CUtensorMapDataType)dtype, 2, const_cast<void*>(base), dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
 // Launch with programmatic stream serialization (PDL): consecutive colour
 // launches overlap one grid's tail with the next grid's prologue.
 template <typename K, typename... Args>
@@ -562,8 +669,28 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   constexpr int R_LO = Op::ARITY <= 2 ? 2 : 4, R_HI = Op::ARITY <= 2 ? 2 : 8;
   const bool hi = P.max_staged > R_LO * nt;
   if (P.max_staged > R_HI * nt) MP_FAIL(MP_ERR_CAPACITY, "block stages %d rows, over %d per CTA", P.max_staged, R_HI * nt);
-  auto kern = dataflow ? (hi ? hier_stream_kernel<Op, T, LAYOUT, true, SlotT, R_HI> : hier_stream_kernel<Op, T, LAYOUT, true, SlotT, R_LO>)
-                       : (hi ? hier_stream_kernel<Op, T, LAYOUT, false, SlotT, R_HI> : hier_stream_kernel<Op, T, LAYOUT, false, SlotT, R_LO>);
+  // staged read rows through TMA gather4 when the rows are 32/64/128-byte
+  // AoS rows with a 16-byte-multiple stride (else LDGSTS gathers)
+  constexpr int QB = Op::RC * (int)sizeof(T);
+  // opt-in (MESHPLAN_STREAM_TMA=1): measured slower than the LDGSTS gathers on
+  // B200 (C5 1.55 vs 1.39 ms; per-lane coordinates serialise through uniform
+  // registers, one gather4 per 4 rows), kept as the TMA-gather variant
+  static const bool env_tma = getenv("MESHPLAN_STREAM_TMA") && atoi(getenv("MESHPLAN_STREAM_TMA")) != 0;
+  CUtensorMap qmap;
+  memset(&qmap, 0, sizeof(qmap));
+  bool tma = false;
+  if constexpr (LAYOUT == MP_AOS && (QB == 32 || QB == 64 || QB == 128)) {  // 4-row groups stay 128-B aligned
+    tma = env_tma && sr && v.n > 0 && (v.ind_comps * (int)sizeof(T)) % 16 == 0 &&
+          (reinterpret_cast<uintptr_t>(v.ind) & 15) == 0;
+    if (tma) MP_CUDA_TRY_DRV(encode_row_map(&qmap, v.ind, (int)sizeof(T), dtype_code<T>(), v.ind_comps, v.npts, Op::RC));
+  }
+  auto pick = [&](auto dflow, auto tmaq) {
+    constexpr bool DF = decltype(dflow)::value, TQ = decltype(tmaq)::value;
+    return hi ? hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_HI, TQ> : hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_LO, TQ>;
+  };
+  using TT = std::true_type;
+  using FF = std::false_type;
+  auto kern = dataflow ? (tma ? pick(TT{}, TT{}) : pick(TT{}, FF{})) : (tma ? pick(FF{}, TT{}) : pick(FF{}, FF{}));
   MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, dev = 0, sms = 0;
   MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
@@ -580,7 +707,7 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
     H.pred_pad = P.tpred_pad;
     H.ntickets = P.num_blocks;
     const int grid = P.num_blocks < resident ? P.num_blocks : resident;
-    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H));
+    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H, qmap));
     return MP_OK;
   }
   for (int c = 0; c < P.num_block_colours; ++c) {
@@ -590,7 +717,7 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
     H.tblock = P.blocks_by_colour + lo;
     H.ntickets = hi - lo;
     const int grid = (hi - lo) < resident ? (hi - lo) : resident;
-    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H));
+    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H, qmap));
   }
   return MP_OK;
 }

@@ -298,3 +298,38 @@ def test_schedules_agree_on_random_data_many_blocks(family, dims, kname, reorder
         out[sched] = t[inc].cpu().numpy()
     for sched in SCHEDULES:
         assert bit_equal(out[sched], out["colour"]), sched
+
+
+def test_stream_tma_gather_variant_matches_colour_schedule():
+    """The opt-in TMA gather4 variant of the streamed executor (read rows
+    through the tensor engine, MESHPLAN_STREAM_TMA=1, read once per process)
+    gives the same bits as the warp-specialised and CTA-per-block executors."""
+    import subprocess
+    import sys
+    import textwrap
+    from pathlib import Path
+
+    code = textwrap.dedent("""
+        import numpy as np, torch, paper_1802_03749_b200 as mp
+        mesh = mp.generate_mesh("quad2d", (300, 260), dtype="f64")
+        kernel = mp.kernel_for_mesh("flux", mesh)
+        plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps"))
+        g = torch.Generator(device="cuda").manual_seed(3)
+        base = {a.array: torch.rand(plan.mesh.data[a.array].values.size, generator=g, device="cuda",
+                                    dtype=torch.float64) for a in kernel.args}
+        out = {}
+        for sched in ("stream", "stream-dataflow", "pipelined", "colour"):
+            t = {k: v.clone() for k, v in base.items()}
+            lp = mp.bind(plan, kernel, tensors=t, schedule=sched)
+            for _ in range(2):
+                lp.run()
+            torch.cuda.synchronize()
+            out[sched] = t["res"].cpu().numpy()
+        for sched in out:
+            assert np.array_equal(out[sched].view(np.uint64), out["colour"].view(np.uint64)), sched
+        print("ok")
+    """)
+    repo = Path(__file__).resolve().parents[1]
+    env = dict(__import__("os").environ, MESHPLAN_STREAM_TMA="1", PYTHONPATH=str(repo))
+    r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
