@@ -91,6 +91,35 @@ def _reorder(mesh, kernel, config, m: Mapping, map_d: torch.Tensor, fwd: dict):
         map_d = pf[map_d[order].long()].to(torch.int32)
         _compose(fwd, m.to_set.name, pf)
         _compose(fwd, iter_set, _fwd_from_order(order))
+    elif mode == "structured" and mesh.meta.get("family", "") == "quad2d":
+        # extension (the reference defines handcrafted blocks for hex meshes
+        # only, plan.py:355-363): bx x by cell tiles of a generated quad grid,
+        # ragged at the far edges; each edge goes with its owner (first) cell
+        # as faces do in partition_structured_hex; points then follow the
+        # writer-set order (reorder.py:174-203) so a tile's cells are contiguous
+        from . import kway
+
+        shape = config.structured_shape()
+        dims = tuple(int(v) for v in str(mesh.meta.get("dims", "")).split())
+        if len(dims) != 2 or shape[2:] not in ((), (1,)):
+            raise MeshValidationError("structured quad2d blocks need a generated quad mesh and bx,by")
+        nx, ny = dims
+        bx, by = shape[0], shape[1]
+        if bx < 1 or by < 1 or npts != nx * ny:
+            raise MeshValidationError(f"block shape {shape} does not fit a {nx}x{ny} quad grid")
+        owner = map_d[:, 0].long()
+        cx, cy = torch.div(owner, ny, rounding_mode="floor"), owner % ny
+        tiles_y = -(-ny // by)
+        assign = torch.div(cx, bx, rounding_mode="floor") * tiles_y + torch.div(cy, by, rounding_mode="floor")
+        order = torch.sort(assign, stable=True).indices
+        counts = torch.bincount(assign, minlength=int(assign.max()) + 1 if assign.numel() else 0)
+        sizes = counts[counts > 0].cpu().numpy().astype(np.int64)
+        dense = torch.cumsum(counts > 0, 0) - 1  # drop empty tiles from the numbering
+        pf = kway.writer_set_forward(map_d, npts, dense[assign])
+        map_d = pf[map_d[order].long()].to(torch.int32)
+        _compose(fwd, m.to_set.name, pf)
+        _compose(fwd, iter_set, _fwd_from_order(order))
+        meta = {"num_blocks": int(sizes.size), "block_shape": [bx, by], "method": "quad2d cell tiles (extension)"}
     elif mode == "structured":
         shape = config.structured_shape()
         family, dims = mesh.meta.get("family", ""), mesh.meta.get("dims", "")

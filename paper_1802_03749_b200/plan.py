@@ -60,7 +60,7 @@ class PlanConfig:
         if not self.reorder.startswith("structured"):
             return None
         parts = self.reorder.partition(":")[2].replace(",", " ").split()
-        if len(parts) != 3:
+        if len(parts) not in (2, 3):  # bx,by: quad2d tiles (extension)
             raise MeshValidationError(f"structured reorder needs bx,by,bz, got {self.reorder!r}")
         return tuple(int(p) for p in parts)
 

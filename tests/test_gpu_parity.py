@@ -333,3 +333,31 @@ def test_stream_tma_gather_variant_matches_colour_schedule():
     env = dict(__import__("os").environ, MESHPLAN_STREAM_TMA="1", PYTHONPATH=str(repo))
     r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("dims,shape,bs", [((96, 83), "8,8", 128), ((61, 40), "4,6", 48), ((50, 50), "8,8,1", 128)])
+def test_quad2d_structured_tiles_extension(dims, shape, bs):
+    """Extension: handcrafted bx x by cell tiles for generated quad meshes
+    (ragged far edges) -- race-free (checked on execute), widths <= S,
+    exact vs the oracle on every schedule, reuse above GPS's."""
+    from oracle import loops
+
+    mesh = mp.generate_mesh("quad2d", dims, dtype="f64")
+    kernel = mp.kernel_for_mesh("flux", mesh)
+    m = mesh.mappings["e2c"]
+    want = loops.serial_loop("flux", m.table, mesh.data["q"].view2d(), np.ascontiguousarray(mesh.data["w"].view2d()),
+                             _v2(mesh, "res"))
+    plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder=f"structured:{shape}", block_size=bs))
+    assert int(np.diff(plan.block_offsets).max()) <= bs
+    for sched in SCHEDULES:
+        res, _ = mp.execute_hierarchical(plan, kernel, schedule=sched)
+        assert bit_equal(_v2(plan.restore_data(res), "res"), want), sched
+    gps = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps", block_size=bs))
+    assert mp.reuse_factor(plan) > mp.reuse_factor(gps)
+
+
+def test_quad2d_structured_rejects_3d_shapes():
+    mesh = mp.generate_mesh("quad2d", (8, 8), dtype="f64")
+    kernel = mp.kernel_for_mesh("flux", mesh)
+    with pytest.raises(mp.MeshValidationError):
+        mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="structured:2,2,2"))
