@@ -113,7 +113,9 @@ typedef struct mp_hier_plan {
    * {first element, elements | thread colours << 16, staged offset, staged
    * count} in blocks_by_colour order and in dataflow order, and one packed
    * record per element: arity local slots (slot_bytes each), the element's
-   * thread colour (1 byte), zero padding to elem_meta_bytes (multiple of 4). */
+   * thread colour (1 byte), a mask of the slots through which the element is
+   * the first writer of its staged row within the block (1 byte, arity <= 8),
+   * zero padding to elem_meta_bytes (multiple of 4). */
   const int32_t* tdesc_colour;    /* [nb][4]                                 */
   const int32_t* tdesc_order;     /* [nb][4]                                 */
   const uint8_t* elem_meta;       /* [n_elems*elem_meta_bytes]               */

@@ -491,12 +491,14 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72)
     T o[A][IC];
     int ls[A];
     int my_tc = -1;
+    unsigned fmask = 0;  // slots whose row this element writes first (store, no load)
     if (t < k) {
       const unsigned char* em = st + L.em + t * H.em_bytes;
       const SlotT* sl = reinterpret_cast<const SlotT*>(em);
 #pragma unroll
       for (int q = 0; q < A; ++q) ls[q] = sl[q];
       my_tc = em[A * sizeof(SlotT)];
+      fmask = em[A * sizeof(SlotT) + 1];
       T dd[DC];
 #pragma unroll
       for (int c = 0; c < DC; ++c) dd[c] = reinterpret_cast<const T*>(st + L.dir)[c * H.max_block + t];
@@ -513,15 +515,21 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72)
 #pragma unroll
         for (int q = 0; q < A; ++q) {
           T acc[IC];
-          lds_row<T, IC>(sh_inc, ls[q], acc);
+          if ((fmask >> q) & 1u) {  // 0 + x, the reference's zeroed shared row (simulator.py:634-643)
 #pragma unroll
-          for (int cc = 0; cc < IC; ++cc) acc[cc] += o[q][cc];
+            for (int cc = 0; cc < IC; ++cc) acc[cc] = o[q][cc] + T(0);
+          } else {
+            lds_row<T, IC>(sh_inc, ls[q], acc);
+#pragma unroll
+            for (int cc = 0; cc < IC; ++cc) acc[cc] += o[q][cc];
+          }
           sts_row<T, IC>(sh_inc, ls[q], acc);
         }
       }
       cbar();
     }
-    // e. write back: row + increment, once per staged row; re-zero the row
+    // e. write back: row + increment, once per staged row (every staged row has
+    //    a first writer, so the shared rows need no re-zeroing)
     if (DATAFLOW && rows_late && t < ns) {
       if (H.stats && t == 0) atomicAdd(H.stats, 1u);
       while (ld_acquire_cta(ctl + 1) <= i) __nanosleep(32);
@@ -551,10 +559,6 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72)
 #pragma unroll
           for (int c = 0; c < IC; ++c) v.inc[(int64_t)c * v.npts + p] = acc[c];
         }
-        T z[IC];
-#pragma unroll
-        for (int c = 0; c < IC; ++c) z[c] = T(0);
-        sts_row<T, IC>(sh_inc, j, z);
       }
     }
     if constexpr (DATAFLOW) {  // this warp's write-back stores are done (release, CTA scope)
@@ -733,8 +737,8 @@ mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool datafl
     if (!P.written_is_staged) MP_FAIL(MP_ERR_KERNEL, "streamed executor needs written lists equal to staged lists");
     if (!P.tdesc_colour || !P.tdesc_order || !P.elem_meta)
       MP_FAIL(MP_ERR_KERNEL, "streamed executor needs the plan's ticket descriptors and element records");
-    if (P.elem_meta_bytes < Op::ARITY * P.slot_bytes + 1 || P.elem_meta_bytes % 4)
-      MP_FAIL(MP_ERR_KERNEL, "element records of %d bytes cannot hold %d slots and a colour", P.elem_meta_bytes,
+    if (Op::ARITY > 8 || P.elem_meta_bytes < Op::ARITY * P.slot_bytes + 2 || P.elem_meta_bytes % 4)
+      MP_FAIL(MP_ERR_KERNEL, "element records of %d bytes cannot hold %d slots, a colour and a first-writer mask", P.elem_meta_bytes,
               Op::ARITY);
     if (dataflow && (!P.order || !P.tpred_offsets || !P.tpreds || !P.tpred_pad || !P.flags))
       MP_FAIL(MP_ERR_KERNEL, "dataflow schedule needs order/preds/flags");

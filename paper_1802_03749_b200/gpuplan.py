@@ -313,7 +313,8 @@ class DevicePlan:
     def finish_stream(self) -> None:
         """Streamed-executor structures: ticket descriptors {e0, k | nc << 16,
         s0, ns} in both schedule orders and packed per-element records (arity
-        local slots, thread colour byte, zero padding to a 4-byte multiple)."""
+        local slots, thread colour byte, first-writer slot mask byte, zero
+        padding to a 4-byte multiple)."""
         nb = self.block_offsets.numel() - 1
         dev = self.meta.device
         base = self.meta.clone()
@@ -347,11 +348,28 @@ class DevicePlan:
         n = int(self.block_offsets[-1]) if nb else 0
         arity = self.map.shape[1]
         sb = self.local_slots.element_size()
-        em = (arity * sb + 1 + 3) & ~3
+        em = (arity * sb + 2 + 3) & ~3
         rec = torch.zeros(n + 4, em, dtype=torch.uint8, device=dev)
         if n:
-            rec[:n, : arity * sb] = self.local_slots[: n * arity].contiguous().view(torch.uint8).view(n, arity * sb)
+            ls = self.local_slots[: n * arity].contiguous()
+            rec[:n, : arity * sb] = ls.view(torch.uint8).view(n, arity * sb)
             rec[:n, arity * sb] = self.thread_colours[:n]
+            if arity <= 8:
+                # first writer of each staged row within its block, in (element,
+                # slot) order = thread-colour order: it stores (0 + x) instead of
+                # adding into a zeroed row
+                slot = (ls.view(torch.int16).long() & 0xFFFF) if sb == 2 else ls.long()
+                sizes = (self.block_offsets[1:] - self.block_offsets[:-1]).long()
+                blk = torch.repeat_interleave(torch.arange(nb, device=dev), sizes * arity)
+                key = blk * (int(self.max_staged) + 2) + slot
+                order = torch.sort(key, stable=True).indices
+                sk = key[order]
+                first_sorted = torch.ones_like(sk, dtype=torch.bool)
+                first_sorted[1:] = sk[1:] != sk[:-1]
+                first = torch.zeros(n * arity, dtype=torch.bool, device=dev)
+                first[order] = first_sorted
+                bits = (first.view(n, arity).long() << torch.arange(arity, device=dev)).sum(1)
+                rec[:n, arity * sb + 1] = bits.to(torch.uint8)
         self.elem_meta = rec.reshape(-1)
         self.elem_meta_bytes = em
 
