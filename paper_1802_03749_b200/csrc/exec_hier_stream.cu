@@ -50,6 +50,10 @@
 
 #include "mp_loop.cuh"
 
+#ifndef MP_STREAM_MAXREG
+#define MP_STREAM_MAXREG 72  // 7 CTAs of 128 threads per SM
+#endif
+
 namespace mp {
 namespace {
 
@@ -153,8 +157,8 @@ struct RowFmt {
   static constexpr int N = RB / G;
   static constexpr bool SWZ = G == 16 && N >= 2 && N <= 8 && (N & (N - 1)) == 0;
   static constexpr int PITCH = RB == 0 ? 0 : ((N % 2 == 1 || SWZ) ? RB : RB + G);
-  static constexpr int SHIFT = SWZ ? (N == 2 ? 2 : (N == 4 ? 1 : 0)) : 0;
   __device__ __forceinline__ static int slot(int r, int c) {
+    constexpr int SHIFT = N == 2 ? 2 : (N == 4 ? 1 : 0);
     if constexpr (SWZ) return r * PITCH + ((c ^ ((r >> SHIFT) & (N - 1))) * G);
     else return r * PITCH + c * G;
   }
@@ -247,29 +251,32 @@ struct StreamLayout {
   static constexpr int QP = RowFmt<QB>::PITCH, IP = RowFmt<IB>::PITCH;
   int ids, q, dir, em, bytes, inc, ctl, total;
   __host__ __device__ static int a16(int x) { return (x + 15) & ~15; }
-  __host__ __device__ StreamLayout(int ms, int mb, int em_bytes, bool stage_reads, int nstage) {
-    const int qrows = Op::RC == 0 ? 0 : (stage_reads ? ms : mb * Op::ARITY);
+  // stage_reads: staged read rows [ms (+3)][QP]; increment-only staging: the
+  // block's mapping rows [mb][ARITY] int32 (reads go straight to registers).
+  // tma: 1024-byte aligned read rows (TMA swizzle atoms)
+  __host__ __device__ StreamLayout(int ms, int mb, int em_bytes, bool stage_reads, int nstage, bool tma = false) {
+    const int qbytes = Op::RC == 0 ? 0 : (stage_reads ? ((ms + 3) & ~3) * QP : mb * Op::ARITY * 4);
+    const int al = tma ? 1023 : 15;
     ids = 16;
-    q = (ids + ms * 4 + 1023) & ~1023;  // swizzle atoms (TMA) need 1024-B alignment
-    dir = a16(q + ((qrows + 3) & ~3) * QP);
+    q = (ids + ms * 4 + al) & ~al;
+    dir = a16(q + qbytes);
     em = a16(dir + Op::DC * mb * (int)sizeof(T));
-    bytes = a16(em + mb * em_bytes);
-    bytes = (bytes + 1023) & ~1023;
+    bytes = (em + mb * em_bytes + al) & ~al;
     inc = nstage * bytes;
     ctl = a16(inc + ms * IP);
     total = ctl + CTL_BYTES;
   }
 };
 
-template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR, bool TMAQ>
-__global__ void __maxnreg__(DATAFLOW ? 64 : 72)
+template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR, bool TMAQ, bool SR>
+__global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
     hier_stream_kernel(LoopView<T> v, StreamView H, const __grid_constant__ CUtensorMap qmap) {
   constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
   using L_t = StreamLayout<Op, T>;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int NT = H.nt, D = H.depth, NS = H.depth + 1;
-  const bool stage_reads = RC > 0 && H.stage_reads != 0;
-  const L_t L(H.max_staged, H.max_block, H.em_bytes, stage_reads, NS);
+  constexpr bool stage_reads = RC > 0 && SR;  // staged read rows (else reads via the mapping)
+  const L_t L(H.max_staged, H.max_block, H.em_bytes, stage_reads, NS, TMAQ);
   unsigned char* sh_inc = smem + L.inc;
   int* ctl = reinterpret_cast<int*>(smem + L.ctl);  // [0] done count, [1] ready count
   const int tid = threadIdx.x;
@@ -419,10 +426,10 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72)
       } else {
         for (int o = 0; o < H.em_bytes; o += 4) cpa<4>(dst + o, src + o);
       }
-      if (RC > 0 && !stage_reads) {
+    }
+    if (RC > 0 && !stage_reads && t < H.max_block) {  // this thread's own mapping row (-1: no element)
 #pragma unroll
-        for (int sl = 0; sl < A; ++sl) gather_row<T, RCN, LAYOUT>(st + L.q, t * A + sl, v.ind, mp[sl], v.ind_comps, v.npts);
-      }
+      for (int sl = 0; sl < A; ++sl) reinterpret_cast<int*>(st + L.q)[t * A + sl] = t < k ? mp[sl] : -1;
     }
   };
   // increment rows of block f (staged ids of stage s) -> registers; on the
@@ -476,6 +483,18 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72)
     const int4 d_next = load_desc(i + D + 1);
     load_ids(d_fill, ids_fill);
     load_map(d_fill, map_fill);
+    // increment-only staging: this thread's element reads through its own
+    // mapping row (stored by this thread at fill time), issued before the wait
+    T r[A][RCN];
+    if constexpr (RC > 0 && !stage_reads) if (t < H.max_block) {
+      const int* mrow = reinterpret_cast<const int*>(smem + s * L.bytes + L.q) + t * A;
+#pragma unroll
+      for (int q = 0; q < A; ++q) {
+        const int p = max(mrow[q], 0);
+#pragma unroll
+        for (int c = 0; c < RCN; ++c) r[q][c] = __ldg(v.ind + ind_index<LAYOUT>(p, c, v.ind_comps, v.npts));
+      }
+    }
     // b. block i has landed (D-1 younger groups may still be in flight)
     cp_wait(D - 1);
     if constexpr (TMAQ) {
@@ -502,10 +521,9 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : 72)
       T dd[DC];
 #pragma unroll
       for (int c = 0; c < DC; ++c) dd[c] = reinterpret_cast<const T*>(st + L.dir)[c * H.max_block + t];
-      T r[A][RCN];
-      if constexpr (RC > 0) {
+      if (RC > 0 && stage_reads) {
 #pragma unroll
-        for (int q = 0; q < A; ++q) lds_row<T, RCN>(st + L.q, stage_reads ? ls[q] : t * A + q, r[q]);
+        for (int q = 0; q < A; ++q) lds_row<T, RCN>(st + L.q, ls[q], r[q]);
       }
       compute<Op, T>(v, r, dd, o);
     }
@@ -640,8 +658,14 @@ template <class Op, typename T, int LAYOUT, typename SlotT>
 mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
   static const int env_depth = getenv("MESHPLAN_STREAM_DEPTH") ? atoi(getenv("MESHPLAN_STREAM_DEPTH")) : 2;
   static const int env_ctas = getenv("MESHPLAN_STREAM_CTAS") ? atoi(getenv("MESHPLAN_STREAM_CTAS")) : 0;
-  int depth = env_depth < 1 ? 1 : (env_depth > 4 ? 4 : env_depth);
-  const int nt = ((P.block_size + 31) / 32) * 32;
+  int depth = env_depth < 2 ? 2 : (env_depth > 4 ? 4 : env_depth);
+  // CTA width: one thread per block element, widened (idle in the element
+  // phases) when the widest staged list would need more than R_LO rows per
+  // thread -- arity-8 loops stage ~4 rows per element
+  constexpr int R_LO0 = Op::ARITY <= 2 ? 2 : 4;
+  int nt = ((P.block_size + 31) / 32) * 32;
+  const int nt_rows = ((P.max_staged + R_LO0 - 1) / R_LO0 + 31) / 32 * 32;
+  if (nt_rows > nt) nt = nt_rows < 480 ? nt_rows : 480;
   H.nt = nt;
   H.max_block = P.block_size;
   H.max_staged = P.max_staged;
@@ -658,21 +682,6 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   }
   H.stats = stats;
   const bool sr = Op::RC > 0 && P.stage_reads;
-  size_t smem = 0;
-  for (;; --depth) {  // shrink the ring if it does not fit
-    const StreamLayout<Op, T> L(P.max_staged, P.block_size, P.elem_meta_bytes, sr, depth + 1);
-    smem = (size_t)L.total;
-    if (smem <= 227 * 1024 || depth == 1) break;
-  }
-  if (smem > 227 * 1024)
-    MP_FAIL(MP_ERR_CAPACITY, "streamed executor needs %zu shared bytes, over the 232448-byte limit", smem);
-  H.depth = depth;
-  const int threads = nt + (dataflow ? 32 : 0);
-  if (threads > 512) MP_FAIL(MP_ERR_CAPACITY, "block size %d exceeds the streamed executor limit of 480", P.block_size);
-  // staged rows per thread (ns <= ARITY * k): 2 for pair loops, 4 or 8 otherwise
-  constexpr int R_LO = Op::ARITY <= 2 ? 2 : 4, R_HI = Op::ARITY <= 2 ? 2 : 8;
-  const bool hi = P.max_staged > R_LO * nt;
-  if (P.max_staged > R_HI * nt) MP_FAIL(MP_ERR_CAPACITY, "block stages %d rows, over %d per CTA", P.max_staged, R_HI * nt);
   // staged read rows through TMA gather4 when the rows are 32/64/128-byte
   // AoS rows with a 16-byte-multiple stride (else LDGSTS gathers)
   constexpr int QB = Op::RC * (int)sizeof(T);
@@ -688,13 +697,35 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
           (reinterpret_cast<uintptr_t>(v.ind) & 15) == 0;
     if (tma) MP_CUDA_TRY_DRV(encode_row_map(&qmap, v.ind, (int)sizeof(T), dtype_code<T>(), v.ind_comps, v.npts, Op::RC));
   }
-  auto pick = [&](auto dflow, auto tmaq) {
-    constexpr bool DF = decltype(dflow)::value, TQ = decltype(tmaq)::value;
-    return hi ? hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_HI, TQ> : hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_LO, TQ>;
-  };
+  size_t smem = 0;
+  for (;; --depth) {  // shrink the ring if it does not fit
+    const StreamLayout<Op, T> L(P.max_staged, P.block_size, P.elem_meta_bytes, sr, depth + 1, tma);
+    smem = (size_t)L.total;
+    if (smem <= 227 * 1024 || depth == 2) break;
+  }
+  if (smem > 227 * 1024)
+    MP_FAIL(MP_ERR_CAPACITY, "streamed executor needs %zu shared bytes, over the 232448-byte limit", smem);
+  H.depth = depth;
+  const int threads = nt + (dataflow ? 32 : 0);
+  if (threads > 512) MP_FAIL(MP_ERR_CAPACITY, "block size %d exceeds the streamed executor limit of 480", P.block_size);
+  // staged rows per thread (ns <= ARITY * k): 2 for pair loops, 4 or 8 otherwise
+  constexpr int R_LO = Op::ARITY <= 2 ? 2 : 4, R_HI = Op::ARITY <= 2 ? 2 : 8;
+  const bool hi = P.max_staged > R_LO * nt;
+  if (P.max_staged > R_HI * nt) MP_FAIL(MP_ERR_CAPACITY, "block stages %d rows, over %d per CTA", P.max_staged, R_HI * nt);
   using TT = std::true_type;
   using FF = std::false_type;
-  auto kern = dataflow ? (tma ? pick(TT{}, TT{}) : pick(TT{}, FF{})) : (tma ? pick(FF{}, TT{}) : pick(FF{}, FF{}));
+  constexpr bool TMA_OK = LAYOUT == MP_AOS && (QB == 32 || QB == 64 || QB == 128);
+  auto pick_r = [&](auto dflow, auto tmaq, auto sread) {
+    constexpr bool DF = decltype(dflow)::value, TQ = decltype(tmaq)::value, S = decltype(sread)::value;
+    return hi ? hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_HI, TQ, S>
+              : hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_LO, TQ, S>;
+  };
+  auto pick = [&](auto dflow) {
+    if constexpr (Op::RC == 0) return pick_r(dflow, FF{}, FF{});
+    else if constexpr (TMA_OK) return tma ? pick_r(dflow, TT{}, TT{}) : (sr ? pick_r(dflow, FF{}, TT{}) : pick_r(dflow, FF{}, FF{}));
+    else return sr ? pick_r(dflow, FF{}, TT{}) : pick_r(dflow, FF{}, FF{});
+  };
+  auto kern = dataflow ? pick(TT{}) : pick(FF{});
   MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, dev = 0, sms = 0;
   MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
