@@ -345,7 +345,7 @@ def our_arm(args):
     prof = REPO / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(f"{args.config}:{args.reorder}:{args.schedule}")
+            traffic = json.loads(prof.read_text()).get(f"{args.config}:{args.reorder}:{args.schedule}")  # per step
         except Exception:
             traffic = None
     line = {

@@ -230,6 +230,14 @@ class DistributedLoop:
         self.loop.run()
         self.halo.export_increments(self.loop.tensors[self.inc], self.ic)
 
+    def step_host(self, inputs: dict, out) -> None:
+        """One end-to-end step with host buffers: H2D of this rank's local
+        arrays (pinned), the decomposed step, D2H of the increment array."""
+        self.loop.run_host_inputs(inputs)
+        self.step()
+        inc = self.loop.tensors[self.inc]
+        out.copy_(inc.reshape(out.shape), non_blocking=True)
+
     def owned_result(self) -> np.ndarray:
         """Owned rows of the increment array, in the decomposition's (global) order."""
         pf = self.plan.set_perms[next(iter(self.plan.mesh.mappings.values())).to_set.name].forward
@@ -293,6 +301,8 @@ def bench_rank(args, rank: int, world: int) -> int:
     sched = "stream" if args.schedule == "best" else args.schedule
     dl = DistributedLoop(mesh, kernel, dec, TorchDistTransport(), cfg, sched)
     t_plan = time.perf_counter() - t0
+    sampler = bench.ClockSampler(local_rank)
+    sampler.start()
     for _ in range(args.warmup):
         dl.step()
     torch.cuda.synchronize()
@@ -307,6 +317,28 @@ def bench_rank(args, rank: int, world: int) -> int:
     dist.barrier()
     ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    clocks = sampler.stop()
+    # end to end: pinned host copies of this rank's arrays -> H2D -> step -> D2H
+    host = {}
+    for name, tns in dl.loop.tensors.items():
+        h = torch.empty(tns.numel(), dtype=tns.dtype, pin_memory=True)
+        h.copy_(tns.reshape(-1))
+        host[name] = h
+    out = torch.empty(dl.loop.tensors[dl.inc].numel(), dtype=dl.loop.tensors[dl.inc].dtype, pin_memory=True)
+    h2d = sum(h.numel() * h.element_size() for h in host.values())
+    d2h = out.numel() * out.element_size()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a.record()
+    n_e2e = max(3, args.steps // 2)
+    for _ in range(n_e2e):
+        dl.step_host(host, out)
+    b.record()
+    torch.cuda.synchronize()
+    ms_e2e = torch.tensor([a.elapsed_time(b) / n_e2e], device=dev)
+    dist.all_reduce(ms_e2e, op=dist.ReduceOp.MAX)
+    io = torch.tensor([h2d, d2h], dtype=torch.float64, device=dev)
+    dist.all_reduce(io)
     n_edges = nx * (ny - 1) + ny * (nx - 1)
     ub_total = nx * ny * 4 * 8 * 3 + n_edges * (2 * 8 + 2 * 4)
     peak, kind = bench.hbm_peak()
@@ -323,7 +355,12 @@ def bench_rank(args, rank: int, world: int) -> int:
             "roofline": {"bound": "hbm", "achieved": round(gbps / world, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(gbps / world / peak, 4), "traffic": None, "peak_kind": kind,
                          "note": "per-GPU share of the whole-job effective bandwidth"},
+            "e2e": {"value": round(ub_total / (float(ms_e2e) * 1e-3) / 1e9, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(io[0]), "d2h_bytes_per_step": int(io[1]),
+                    "ms_per_step": round(float(ms_e2e), 3),
+                    "path": "DistributedLoop.step_host on every rank: pinned local arrays -> H2D -> halo + loop -> D2H"},
             "gpu_launches": int(args.steps * dl.launches_per_step()),
+            "clocks": clocks,
             "cpu_baseline": None, "plan_build_s": round(t_plan, 2),
         }
         print(json.dumps(line), flush=True)

@@ -182,6 +182,17 @@ class DeviceLoop:
                   "mp_exec_hier_pipelined" if self.pipelined else "mp_exec_hier")
             _native.call(fn, self.loop, dp.struct_cached(), self.schedule, max(dp.epoch, 1), sp)
 
+    def run_host_inputs(self, inputs: dict) -> None:
+        """Asynchronous H2D of the given arrays (name -> pinned numpy / torch,
+        plan numbering) into the bound device tensors."""
+        import warnings
+
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)  # read-only numpy views of pinned buffers
+            for name, host in inputs.items():
+                src = torch.from_numpy(host) if isinstance(host, np.ndarray) else host
+                self.tensors[name].copy_(src.reshape(self.tensors[name].shape), non_blocking=True)
+
     def run_host(self, inputs: dict, out, stream=None) -> None:
         """One end-to-end step with host buffers: H2D of the given arrays
         (name -> pinned numpy / torch, plan numbering), the launch, and D2H of
