@@ -46,7 +46,7 @@ CONFIGS = {
     "C5": ("quad2d", (5657, 5657), "flux", "f64", "all-indirect"),
 }
 METRIC = "effective HBM GB/s and ms/iter per indirect loop vs global colouring, 1/2/4/8 GPU"
-SCHEDULES = ("stream", "stream-dataflow", "pipelined", "pipelined-pull", "colour", "dataflow")
+SCHEDULES = ("stream", "stream-pull", "stream-dataflow", "pipelined", "pipelined-pull", "colour", "dataflow")
 L2_BYTES = 126 * 2**20
 KERNEL_OF = {"stream": "hier_stream_kernel", "pipelined": "hier_pipe_kernel", "colour": "hier_block_kernel",
              "dataflow": "hier_block_kernel"}

@@ -67,6 +67,8 @@ struct StreamView {
   const int32_t* __restrict__ pred_pad;  // [ntickets][8] (dataflow)
   uint32_t* flags;
   uint32_t epoch;
+  const uint16_t* __restrict__ pull_off;  // pull variant: plan pull lists
+  const uint16_t* __restrict__ pull_ref;
   int32_t ntickets;
   int32_t em_bytes;
   int32_t max_staged;
@@ -244,31 +246,57 @@ constexpr int CTL_RING = 8;
 constexpr int MAX_NS = 6;
 constexpr int CTL_BYTES = CTL_RING * 4 + MAX_NS * 8;
 
+// registers -> global row (point p) of the incremented array
+template <typename T, int NC, int LAYOUT>
+__device__ __forceinline__ void stg_row(T* g, int64_t p, int64_t npts, const T (&in)[NC]) {
+  if constexpr (LAYOUT == MP_AOS) {
+    constexpr int RB = NC * (int)sizeof(T);
+    constexpr int GG = RB % 16 == 0 ? 16 : (RB % 8 == 0 ? 8 : 4);
+    using V = typename Gran<GG>::type;
+    unsigned char* dst = reinterpret_cast<unsigned char*>(g + p * NC);
+#pragma unroll
+    for (int ch = 0; ch < RB / GG; ++ch) {
+      V x;
+      memcpy(&x, reinterpret_cast<const unsigned char*>(in) + ch * GG, GG);
+      *reinterpret_cast<V*>(dst + ch * GG) = x;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) g[(int64_t)c * npts + p] = in[c];
+  }
+}
+
 // Stage layout (bytes), identical on host and device.
 template <class Op, typename T>
 struct StreamLayout {
   static constexpr int QB = RcArr<Op>::N * (int)sizeof(T), IB = Op::IC * (int)sizeof(T);
   static constexpr int QP = RowFmt<QB>::PITCH, IP = RowFmt<IB>::PITCH;
-  int ids, q, dir, em, bytes, inc, ctl, total;
+  int ids, q, dir, em, poff, pref, bytes, inc, ctl, total;
   __host__ __device__ static int a16(int x) { return (x + 15) & ~15; }
   // stage_reads: staged read rows [ms (+3)][QP]; increment-only staging: the
   // block's mapping rows [mb][ARITY] int32 (reads go straight to registers).
-  // tma: 1024-byte aligned read rows (TMA swizzle atoms)
-  __host__ __device__ StreamLayout(int ms, int mb, int em_bytes, bool stage_reads, int nstage, bool tma = false) {
+  // tma: 1024-byte aligned read rows (TMA swizzle atoms).  pull: the block's
+  // pull lists (u16 offsets per staged row, u16 refs per (element, slot),
+  // 4-byte windows) and a parking buffer [mb*ARITY][IP] instead of the
+  // shared increment rows [ms][IP].
+  __host__ __device__ StreamLayout(int ms, int mb, int em_bytes, bool stage_reads, int nstage, bool tma = false,
+                                   bool pull = false) {
     const int qbytes = Op::RC == 0 ? 0 : (stage_reads ? ((ms + 3) & ~3) * QP : mb * Op::ARITY * 4);
     const int al = tma ? 1023 : 15;
     ids = 16;
     q = (ids + ms * 4 + al) & ~al;
     dir = a16(q + qbytes);
     em = a16(dir + Op::DC * mb * (int)sizeof(T));
-    bytes = (em + mb * em_bytes + al) & ~al;
+    poff = a16(em + mb * em_bytes);
+    pref = a16(poff + (pull ? (ms + 1) * 2 + 8 : 0));
+    bytes = (pref + (pull ? mb * Op::ARITY * 2 + 8 : 0) + al) & ~al;
     inc = nstage * bytes;
-    ctl = a16(inc + ms * IP);
+    ctl = a16(inc + (pull ? mb * Op::ARITY : ms) * IP);
     total = ctl + CTL_BYTES;
   }
 };
 
-template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR, bool TMAQ, bool SR>
+template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR, bool TMAQ, bool SR, bool PULL>
 __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
     hier_stream_kernel(LoopView<T> v, StreamView H, const __grid_constant__ CUtensorMap qmap) {
   constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
@@ -276,7 +304,7 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
   extern __shared__ __align__(1024) unsigned char smem[];
   const int NT = H.nt, D = H.depth, NS = H.depth + 1;
   constexpr bool stage_reads = RC > 0 && SR;  // staged read rows (else reads via the mapping)
-  const L_t L(H.max_staged, H.max_block, H.em_bytes, stage_reads, NS, TMAQ);
+  const L_t L(H.max_staged, H.max_block, H.em_bytes, stage_reads, NS, TMAQ, PULL);
   unsigned char* sh_inc = smem + L.inc;
   int* ctl = reinterpret_cast<int*>(smem + L.ctl);  // [0] done count, [1] ready count
   const int tid = threadIdx.x;
@@ -284,7 +312,7 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
   // static claims: fill f of CTA c takes ticket c + f * grid
   const int total = H.ntickets > (int)blockIdx.x ? (H.ntickets - (int)blockIdx.x + G - 1) / G : 0;
 
-  for (int i = tid; i < H.max_staged * L_t::IP / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sh_inc)[i] = 0u;
+  for (int i = tid; i < (PULL ? 0 : H.max_staged * L_t::IP / 4); i += blockDim.x) reinterpret_cast<uint32_t*>(sh_inc)[i] = 0u;
   if (tid < CTL_RING) ctl[tid] = 0;
   uint64_t* qbar = reinterpret_cast<uint64_t*>(ctl + CTL_RING);  // [NS] staged read rows landed
   if (TMAQ && tid == 0) {
@@ -349,6 +377,7 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
   auto load_desc = [&](int f) -> int4 {
     return f < total ? __ldg(H.tdesc + (int)blockIdx.x + f * G) : make_int4(0, 0, 0, 0);
   };
+  auto load_block = [&](int f) -> int { return (PULL && f < total) ? __ldg(H.tblock + (int)blockIdx.x + f * G) : 0; };
   auto load_ids = [&](const int4& d, int (&ids)[MAXR]) {
 #pragma unroll
     for (int r = 0; r < MAXR; ++r) {  // unpredicated (clamped) loads: no merge copies
@@ -364,9 +393,24 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
     }
   };
   uint64_t row_bits = 0;  // bit s*MAXR + r: this thread's row r of the block in stage s exists
-  auto issue_fill = [&](int s, const int4& d, const int (&ids)[MAXR], const int (&mp)[A]) {
+  auto issue_fill = [&](int s, const int4& d, int blk, const int (&ids)[MAXR], const int (&mp)[A]) {
     unsigned char* st = smem + s * L.bytes;
     const int k = d.y & 0xffff, ns = d.w;
+    if constexpr (PULL) {  // 4-byte windows over the u16 lists; the u16 deltas go to the header
+      const int64_t ob = ((int64_t)d.z + blk) * 2, olo = ob & ~int64_t(3);
+      const int ow = ns > 0 ? (int)((ob - olo) + (ns + 1) * 2 + 3) / 4 : 0;
+      const int64_t rb = (int64_t)d.x * A * 2, rlo = rb & ~int64_t(3);
+      const int rw = k > 0 ? (int)((rb - rlo) + k * A * 2 + 3) / 4 : 0;
+      for (int w = t; w < ow + rw; w += NT) {
+        if (w < ow)
+          cpa<4>(st + L.poff + 4 * w, reinterpret_cast<const unsigned char*>(H.pull_off) + olo + 4 * w);
+        else
+          cpa<4>(st + L.pref + 4 * (w - ow), reinterpret_cast<const unsigned char*>(H.pull_ref) + rlo + 4 * (w - ow));
+      }
+      if (t == 0) {
+        reinterpret_cast<int*>(st)[3] = (int)(ob - olo) / 2 | ((int)(rb - rlo) / 2) << 16;
+      }
+    }
     uint64_t bits = 0;
 #pragma unroll
     for (int r = 0; r < MAXR; ++r) bits |= (uint64_t)(t + r * NT < ns) << r;
@@ -463,10 +507,11 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
     const int4 d = load_desc(f);
     load_ids(d, ids_fill);
     load_map(d, map_fill);
-    issue_fill(f, d, ids_fill, map_fill);
+    issue_fill(f, d, load_block(f), ids_fill, map_fill);
     cp_commit();
   }
   int4 d_fill = load_desc(D);
+  int b_fill = load_block(D);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous launch's increments are visible
   load_rows(0, 0);  // the ids are this thread's own shared stores: no wait
 
@@ -481,6 +526,7 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
   for (int i = 0; i < total; ++i) {
     // a. loads for the bottom of this iteration and the next one
     const int4 d_next = load_desc(i + D + 1);
+    const int b_next = load_block(i + D + 1);
     load_ids(d_fill, ids_fill);
     load_map(d_fill, map_fill);
     // increment-only staging: this thread's element reads through its own
@@ -527,6 +573,45 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
       }
       compute<Op, T>(v, r, dd, o);
     }
+    if constexpr (PULL) {
+      // d'. pull form of the colour loop: park every element's increments
+      //     (one barrier), then the owner of staged row j sums the row's refs
+      //     in thread-colour order starting from 0 -- the reference's zeroed
+      //     shared row + per-colour np.add.at (simulator.py:634-643), bit for
+      //     bit -- and writes row + sum back once.
+      if (t < k) {
+#pragma unroll
+        for (int q = 0; q < A; ++q) sts_row<T, IC>(sh_inc, t * A + q, o[q]);
+      }
+      cbar();
+      const int dl = hdr[3];
+      const uint16_t* po = reinterpret_cast<const uint16_t*>(st + L.poff) + (dl & 0xffff);
+      const uint16_t* pr = reinterpret_cast<const uint16_t*>(st + L.pref) + (dl >> 16);
+      if (DATAFLOW && rows_late && t < ns) {
+        while (ld_acquire_cta(ctl + 1) <= i) __nanosleep(32);
+      }
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        const int j = t + r * NT;
+        if (j < ns) {
+          const int64_t p = reinterpret_cast<const int*>(st + L.ids)[j];
+          const int lo = po[j], hi = po[j + 1];
+          T acc[IC], x[IC];
+          lds_row<T, IC>(sh_inc, pr[lo], x);
+#pragma unroll
+          for (int c = 0; c < IC; ++c) acc[c] = x[c] + T(0);  // 0 + x
+          for (int rr = lo + 1; rr < hi; ++rr) {
+            lds_row<T, IC>(sh_inc, pr[rr], x);
+#pragma unroll
+            for (int c = 0; c < IC; ++c) acc[c] += x[c];
+          }
+          if (DATAFLOW && rows_late) ldg_row<T, IC, LAYOUT>(v.inc, p, v.npts, true, rrow[r]);
+#pragma unroll
+          for (int c = 0; c < IC; ++c) acc[c] = rrow[r][c] + acc[c];
+          stg_row<T, IC, LAYOUT>(v.inc, p, v.npts, acc);
+        }
+      }
+    } else {
     // d. thread colours, one at a time
     for (int c = 0; c < nc; ++c) {
       if (my_tc == c) {
@@ -579,6 +664,7 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
         }
       }
     }
+    }  // push form
     if constexpr (DATAFLOW) {  // this warp's write-back stores are done (release, CTA scope)
       __syncwarp();
       if ((t & 31) == 0) red_release_cta_add(ctl + 0, 1);
@@ -586,11 +672,12 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
     // f. issue fill i+D into the stage block i-1 used (every thread passed
     //    this iteration's barrier after finishing block i-1); load block
     //    i+1's increment rows (its ids were stored by this thread)
-    issue_fill(s_fill, d_fill, ids_fill, map_fill);
+    issue_fill(s_fill, d_fill, b_fill, ids_fill, map_fill);
     cp_commit();
     const int s_next = s + 1 == NS ? 0 : s + 1;
     load_rows(i + 1, s_next);
     d_fill = d_next;
+    b_fill = b_next;
     s_fill = s;
     s = s_next;
   }
@@ -655,7 +742,8 @@ cudaError_t launch_pdl(K kern, int grid, int threads, size_t smem, cudaStream_t 
 }
 
 template <class Op, typename T, int LAYOUT, typename SlotT>
-mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
+mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& P, bool dataflow, bool pull,
+                        cudaStream_t st) {
   static const int env_depth = getenv("MESHPLAN_STREAM_DEPTH") ? atoi(getenv("MESHPLAN_STREAM_DEPTH")) : 2;
   static const int env_ctas = getenv("MESHPLAN_STREAM_CTAS") ? atoi(getenv("MESHPLAN_STREAM_CTAS")) : 0;
   int depth = env_depth < 2 ? 2 : (env_depth > 4 ? 4 : env_depth);
@@ -699,7 +787,7 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   }
   size_t smem = 0;
   for (;; --depth) {  // shrink the ring if it does not fit
-    const StreamLayout<Op, T> L(P.max_staged, P.block_size, P.elem_meta_bytes, sr, depth + 1, tma);
+    const StreamLayout<Op, T> L(P.max_staged, P.block_size, P.elem_meta_bytes, sr, depth + 1, tma, pull);
     smem = (size_t)L.total;
     if (smem <= 227 * 1024 || depth == 2) break;
   }
@@ -715,17 +803,20 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   using TT = std::true_type;
   using FF = std::false_type;
   constexpr bool TMA_OK = LAYOUT == MP_AOS && (QB == 32 || QB == 64 || QB == 128);
-  auto pick_r = [&](auto dflow, auto tmaq, auto sread) {
-    constexpr bool DF = decltype(dflow)::value, TQ = decltype(tmaq)::value, S = decltype(sread)::value;
-    return hi ? hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_HI, TQ, S>
-              : hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_LO, TQ, S>;
+  auto pick_r = [&](auto dflow, auto tmaq, auto sread, auto pl) {
+    constexpr bool DF = decltype(dflow)::value, TQ = decltype(tmaq)::value, S = decltype(sread)::value,
+                   PU = decltype(pl)::value;
+    return hi ? hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_HI, TQ, S, PU>
+              : hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_LO, TQ, S, PU>;
   };
-  auto pick = [&](auto dflow) {
-    if constexpr (Op::RC == 0) return pick_r(dflow, FF{}, FF{});
-    else if constexpr (TMA_OK) return tma ? pick_r(dflow, TT{}, TT{}) : (sr ? pick_r(dflow, FF{}, TT{}) : pick_r(dflow, FF{}, FF{}));
-    else return sr ? pick_r(dflow, FF{}, TT{}) : pick_r(dflow, FF{}, FF{});
+  auto pick_s = [&](auto dflow, auto pl) {  // staging-mode / TMA variants
+    if constexpr (Op::RC == 0) return pick_r(dflow, FF{}, FF{}, pl);
+    else if constexpr (TMA_OK && !decltype(pl)::value)
+      return tma ? pick_r(dflow, TT{}, TT{}, pl) : (sr ? pick_r(dflow, FF{}, TT{}, pl) : pick_r(dflow, FF{}, FF{}, pl));
+    else return sr ? pick_r(dflow, FF{}, TT{}, pl) : pick_r(dflow, FF{}, FF{}, pl);
   };
-  auto kern = dataflow ? pick(TT{}) : pick(FF{});
+  // pull form: colour schedule only
+  auto kern = dataflow ? pick_s(TT{}, FF{}) : (pull ? pick_s(FF{}, TT{}) : pick_s(FF{}, FF{}));
   MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, dev = 0, sms = 0;
   MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
@@ -758,7 +849,8 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
 }
 
 template <class Op, typename T>
-mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool dataflow, uint32_t epoch, cudaStream_t st) {
+mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool dataflow, bool pull, uint32_t epoch,
+                           cudaStream_t st) {
   if constexpr (!op_supported<Op, T>()) {
     MP_FAIL(MP_ERR_KERNEL, "heavy face flux needs float data");
   } else {
@@ -775,6 +867,8 @@ mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool datafl
       MP_FAIL(MP_ERR_KERNEL, "dataflow schedule needs order/preds/flags");
     StreamView H{};
     H.staged_ids = P.staged_ids;
+    H.pull_off = P.pull_off;
+    H.pull_ref = P.pull_ref;
     H.emeta = P.elem_meta;
     H.pred_offsets = P.pred_offsets;
     H.preds = P.preds;
@@ -784,11 +878,11 @@ mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool datafl
     LoopView<T> v = make_view<T>(Lp);
     const bool u8 = P.slot_bytes == 1;
     if (Lp.ind_layout == MP_AOS) {
-      if (u8) return launch_stream<Op, T, MP_AOS, uint8_t>(v, H, P, dataflow, st);
-      return launch_stream<Op, T, MP_AOS, uint16_t>(v, H, P, dataflow, st);
+      if (u8) return launch_stream<Op, T, MP_AOS, uint8_t>(v, H, P, dataflow, pull, st);
+      return launch_stream<Op, T, MP_AOS, uint16_t>(v, H, P, dataflow, pull, st);
     }
-    if (u8) return launch_stream<Op, T, MP_SOA, uint8_t>(v, H, P, dataflow, st);
-    return launch_stream<Op, T, MP_SOA, uint16_t>(v, H, P, dataflow, st);
+    if (u8) return launch_stream<Op, T, MP_SOA, uint8_t>(v, H, P, dataflow, pull, st);
+    return launch_stream<Op, T, MP_SOA, uint16_t>(v, H, P, dataflow, pull, st);
   }
 }
 
@@ -800,11 +894,13 @@ extern "C" mp_status mp_exec_hier_stream(const mp_loop* loop, const mp_hier_plan
   mp::clear_error();
   if (!loop || !plan) MP_FAIL(MP_ERR_KERNEL, "null argument");
   const bool df = (schedule & 3) == MP_SCHED_DATAFLOW;
+  const bool pull = !df && (schedule & MP_SCHED_PULL) != 0;
+  if (pull && (!plan->pull_off || !plan->pull_ref)) MP_FAIL(MP_ERR_KERNEL, "pull form needs the plan's pull lists");
   if (df && epoch == 0) MP_FAIL(MP_ERR_KERNEL, "dataflow epochs start at 1");
   cudaStream_t st = mp::as_stream(stream);
   const mp_loop& L = *loop;
   const mp_hier_plan& P = *plan;
   return MP_DISPATCH_OP(L.op, [&]() {
-    return MP_DISPATCH_DTYPE(L.dtype, [&]() { return mp::launch_stream_op<Op, scalar_t>(L, P, df, epoch, st); });
+    return MP_DISPATCH_DTYPE(L.dtype, [&]() { return mp::launch_stream_op<Op, scalar_t>(L, P, df, pull, epoch, st); });
   });
 }

@@ -34,6 +34,7 @@ SCHEDULES = {
     "pipelined-dataflow-pull": (_native.MP_SCHED_DATAFLOW | _native.MP_SCHED_PULL, True),
     "stream": (_native.MP_SCHED_COLOUR, "stream"),
     "stream-dataflow": (_native.MP_SCHED_DATAFLOW, "stream"),
+    "stream-pull": (_native.MP_SCHED_COLOUR | _native.MP_SCHED_PULL, "stream"),
 }
 TORCH_DTYPES = {"f64": torch.float64, "f32": torch.float32, "i64": torch.int64, "i32": torch.int32}
 

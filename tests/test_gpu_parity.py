@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 CASES = golden_cases()
 SCHEDULES = ("dataflow", "colour", "pipelined", "pipelined-dataflow", "pipelined-pull", "pipelined-dataflow-pull",
-             "stream", "stream-dataflow")
+             "stream", "stream-dataflow", "stream-pull")
 
 
 def _ids(c):
