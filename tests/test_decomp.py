@@ -134,8 +134,9 @@ def test_decompose_lists_consistent():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,reorder", [(2, "gps"), (3, "none"), (4, "gps")])
-def test_threaded_ranks_on_one_gpu_match_serial(world, reorder):
+@pytest.mark.parametrize("world,reorder,schedule", [(2, "gps", "dataflow"), (3, "none", "dataflow"),
+                                                    (4, "gps", "stream"), (2, "none", "stream-pull")])
+def test_threaded_ranks_on_one_gpu_match_serial(world, reorder, schedule):
     import threading
 
     import paper_1802_03749_b200 as mp
@@ -164,7 +165,7 @@ def test_threaded_ranks_on_one_gpu_match_serial(world, reorder):
             local = decomp.local_flux_mesh(t, g, dec, q[dec.local_points], w[g], res0)
             kernel = mp.kernel_for_mesh("flux", local)
             dl = decomp.DistributedLoop(local, kernel, dec, decomp.ThreadTransport(hub, r),
-                                        mp.PlanConfig(reorder=reorder, block_size=64))
+                                        mp.PlanConfig(reorder=reorder, block_size=64), schedule)
             for _ in range(3):
                 dl.step()
             torch.cuda.synchronize()
