@@ -18,35 +18,49 @@
 //     so no thread waits on an index load;
 //   * gathers are issued by all lanes (32 rows per warp instruction), row by
 //     row from the block's ascending deduplicated staged list;
-//   * shared rows use an odd number of 16/8/4-byte granules as pitch
-//     (32-byte rows -> 48 bytes), so consecutive slots -- the common case
-//     after GPS / partition reordering -- are bank-conflict free with vector
-//     accesses;
-//   * per-element plan data (slots + thread colour) is one packed record
-//     (plan-time), one 4-byte-granule copy per element.
+//   * shared rows hold an odd number of 16/8/4-byte granules, or are
+//     XOR-swizzled when the granule count is a power of two (32-byte rows),
+//     so consecutive slots -- the common case after GPS / partition
+//     reordering -- are bank-conflict free with vector accesses;
+//   * increment rows are loaded into registers one block ahead (not staged);
+//     the first writer of each staged row stores 0 + x (plan-time mask), so
+//     the shared increment rows are never re-zeroed;
+//   * per-element plan data (slots, thread colour, first-writer mask) is one
+//     packed record (plan-time), one 4-byte-granule copy per element;
+//   * increment-only staging reads the element's rows straight into
+//     registers through its mapping row (issued before the stage wait);
+//   * CTAs are widened when the widest staged list needs more than 2 (4 for
+//     arity 8) rows per thread; 72-register cap -> 7 CTAs of 128 per SM.
 //
-// Schedules: MP_SCHED_COLOUR (one launch per block colour) and
-// MP_SCHED_DATAFLOW (one launch; tickets in a topological order of the
-// lower-colour conflict DAG).  Dataflow adds one "sync" warp per CTA that
+// Schedules: MP_SCHED_COLOUR (one programmatic-dependent launch per block
+// colour: a colour's prologue overlaps the previous colour's tail), its pull
+// form (| MP_SCHED_PULL: elements park their per-slot increments, one
+// barrier, the owner of each staged row sums its refs in thread-colour order
+// from the plan pull lists), and MP_SCHED_DATAFLOW (one launch; tickets in a
+// topological order of the lower-colour conflict DAG).  Dataflow adds one
+// "sync" warp per CTA that
 //   - checks, in fill order and off the critical path, that every
 //     lower-colour predecessor of the CTA's upcoming blocks has written back
-//     (acquire loads of epoch flags) and publishes a ready count in shared
-//     memory; a thread gathers a block's increment rows at fill time only if
-//     the block is already ready, otherwise ("late") it reads them from L2 at
-//     write-back after waiting for readiness;
-//   - releases the flags of the CTA's finished blocks in batches, one gpu
-//     fence per batch (never one fence per block on the compute path).
+//     (relaxed polls of epoch flags from ticket-ordered padded lists, one gpu
+//     fence per productive pass) and publishes a ready count in shared
+//     memory; a block's increment rows are trusted only if the block was
+//     ready when they were loaded, otherwise ("late") they are re-read from
+//     L2 at write-back after waiting for readiness;
+//   - releases the flags of the CTA's finished blocks (per-warp write-back
+//     counters) in batches, one gpu fence per batch.
 // Deadlock freedom: compute threads only wait (late write-back) for the
 // readiness of the block they are writing back, whose predecessors hold
 // smaller tickets; the CTA holding the smallest unfinished ticket has
 // finished all its earlier ones, and sync warps keep releasing finished
 // blocks while they poll, so that ticket always progresses while every CTA
 // is resident (the grid is capped at the occupancy-derived resident count).
+// An opt-in variant (MESHPLAN_STREAM_TMA=1) gathers read rows with TMA
+// tile::gather4 into per-stage mbarriers (measured slower).
 #include <cuda.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <type_traits>
-#include <string.h>
 
 #include "mp_loop.cuh"
 
