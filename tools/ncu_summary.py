@@ -33,7 +33,10 @@ METRICS = [
 
 
 def raw(report: str):
-    out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if report.endswith(".csv"):  # `ncu -i <rep> --page raw --csv` exported on the GPU box
+        out = open(report).read()
+    else:
+        out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return None
