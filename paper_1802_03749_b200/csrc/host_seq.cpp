@@ -16,6 +16,8 @@
 #include <set>
 #include <utility>
 #include <vector>
+#include <cstdint>
+#include <climits>
 
 #include "../../include/meshplan_b200.h"
 
@@ -241,40 +243,78 @@ extern "C" mp_status mp_refine_boundary_pass(int64_t n, const int64_t* indptr, c
 }
 
 // partition.py:255-285 -- push members out of over-cap blocks (best effort).
+//
+// Same decisions as the reference, in O(n + moves * (degree + log nb)):
+// * blocks never become over-cap (a destination must have room), so the
+//   over-cap set only shrinks and its lowest id never decreases, and an
+//   over-cap block never gains members: its member list is the initial one
+//   (ascending, like np.flatnonzero) minus the nodes already moved out;
+// * a candidate's connectivity is 0 unless it is a neighbouring block, so the
+//   reference's lexsort((id, -conn)) picks the best-connected neighbouring
+//   block with room (ties: lowest id) or, when none has room, the lowest-id
+//   block with room -- found with a min segment tree over block weights.
 extern "C" mp_status mp_rebalance(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
                                   int64_t* assignment, int64_t* block_w, int64_t num_blocks, const int64_t* node_w,
                                   int64_t cap, int32_t use_w) {
   mp::clear_error();
-  int64_t guard = 0;
-  std::vector<int64_t> conn(num_blocks), members;
+  if (num_blocks <= 0) return MP_OK;
+  // members per block (counting sort: ascending node ids)
+  std::vector<int64_t> moff(num_blocks + 1, 0), mem(n);
+  for (int64_t u = 0; u < n; ++u) ++moff[assignment[u] + 1];
+  for (int64_t k = 0; k < num_blocks; ++k) moff[k + 1] += moff[k];
+  {
+    std::vector<int64_t> pos(moff.begin(), moff.end() - 1);
+    for (int64_t u = 0; u < n; ++u) mem[pos[assignment[u]]++] = u;
+  }
+  // min segment tree over block weights
+  int64_t size = 1;
+  while (size < num_blocks) size <<= 1;
+  const int64_t INF = INT64_MAX;
+  std::vector<int64_t> tree(2 * size, INF);
+  for (int64_t k = 0; k < num_blocks; ++k) tree[size + k] = block_w[k];
+  for (int64_t i = size - 1; i >= 1; --i) tree[i] = std::min(tree[2 * i], tree[2 * i + 1]);
+  auto update = [&](int64_t k) {
+    int64_t i = size + k;
+    tree[i] = block_w[k];
+    for (i >>= 1; i >= 1; i >>= 1) tree[i] = std::min(tree[2 * i], tree[2 * i + 1]);
+  };
+  auto first_at_most = [&](int64_t limit) -> int64_t {  // lowest k with block_w[k] <= limit
+    if (tree[1] > limit) return -1;
+    int64_t i = 1;
+    while (i < size) i = tree[2 * i] <= limit ? 2 * i : 2 * i + 1;
+    return i - size < num_blocks ? i - size : -1;
+  };
+  std::vector<int64_t> conn(num_blocks, 0), touched;
+  int64_t guard = 0, scan = 0;
   while (true) {
-    int64_t b = -1;
-    for (int64_t k = 0; k < num_blocks; ++k)
-      if (block_w[k] > cap) {
-        b = k;
-        break;
-      }
-    if (b < 0 || guard > n * 4) break;
+    while (scan < num_blocks && block_w[scan] <= cap) ++scan;
+    if (scan >= num_blocks || guard > n * 4) break;
     ++guard;
-    members.clear();
-    for (int64_t u = 0; u < n; ++u)
-      if (assignment[u] == b) members.push_back(u);
+    const int64_t b = scan;
     bool moved = false;
-    for (int64_t u : members) {
+    for (int64_t m = moff[b]; m < moff[b + 1]; ++m) {
+      const int64_t u = mem[m];
+      if (assignment[u] != b) continue;  // moved out in an earlier pass over b
       if (block_w[b] <= cap) break;
-      std::fill(conn.begin(), conn.end(), 0);
-      for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) conn[assignment[indices[j]]] += use_w ? weights[j] : 1;
-      conn[b] = -1;
-      // candidate with the largest connectivity, ties by lowest id, that has room
-      int64_t best = -1;
-      for (int64_t c = 0; c < num_blocks; ++c) {
-        if (c == b || block_w[c] + node_w[u] > cap) continue;
-        if (best < 0 || conn[c] > conn[best]) best = c;
+      touched.clear();
+      for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) {
+        const int64_t c = assignment[indices[j]];
+        if (conn[c] == 0) touched.push_back(c);
+        conn[c] += use_w ? weights[j] : 1;
       }
+      int64_t best = -1;
+      for (int64_t c : touched) {
+        if (c == b || block_w[c] + node_w[u] > cap) continue;
+        if (best < 0 || conn[c] > conn[best] || (conn[c] == conn[best] && c < best)) best = c;
+      }
+      for (int64_t c : touched) conn[c] = 0;
+      if (best < 0) best = first_at_most(cap - node_w[u]);  // lightest-id block with room (b is over cap)
       if (best < 0) continue;
       assignment[u] = best;
       block_w[b] -= node_w[u];
       block_w[best] += node_w[u];
+      update(b);
+      update(best);
       moved = true;
     }
     if (!moved) break;

@@ -14,6 +14,8 @@ and its point reordering (reorder.py:174-203):
 """
 
 import math
+import os
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -152,6 +154,9 @@ def partition_kway(g: ThreadGraph, cfg: PartitionConfig) -> Partition:
     target = max(2 * nb, 64)
     max_cluster = max(1, cap // 4)
     levels = []
+    timing = os.environ.get("MESHPLAN_KWAY_TIMING")
+    t0 = time.perf_counter()
+    tick = (lambda what: print(f"[kway] {what}: {time.perf_counter() - t0:.2f}s", flush=True)) if timing else (lambda what: None)
     while len(node_w) > target:
         visit = rng.permutation(len(node_w)).astype(np.int64)
         match = np.empty(len(node_w), dtype=np.int64)
@@ -162,8 +167,10 @@ def partition_kway(g: ThreadGraph, cfg: PartitionConfig) -> Partition:
             break
         levels.append((indptr, indices, weights, node_w, cmap))
         indptr, indices, weights, node_w = cip, cix, cw_e, cnw
+    tick(f"coarsening ({len(levels)} levels, coarsest {len(node_w)} nodes)")
     assignment = np.empty(len(node_w), dtype=np.int64)
     _native.call("mp_initial_partition", len(node_w), _p(indptr), _p(indices), _p(node_w), nb, cap, _p(assignment))
+    tick("initial partition")
 
     def refine(ip, ix, w, a, nw):
         bw = np.bincount(a, weights=nw, minlength=nb).astype(np.int64)
@@ -182,10 +189,12 @@ def partition_kway(g: ThreadGraph, cfg: PartitionConfig) -> Partition:
                 break
 
     refine(indptr, indices, weights, assignment, node_w)
+    tick("refine coarsest")
     for fip, fix, fw, fnw, cmap in reversed(levels):
         assignment = np.ascontiguousarray(assignment[cmap])
         indptr, indices, weights, node_w = fip, fix, fw, fnw
         refine(indptr, indices, weights, assignment, node_w)
+        tick(f"refine level with {len(fnw)} nodes")
     cut = np.zeros(1, dtype=np.int64)
     gi, gx, gw = (np.ascontiguousarray(a, dtype=np.int64) for a in (g.indptr, g.indices, g.weights))
     _native.call("mp_cut_weight", n, _p(gi), _p(gx), _p(gw), _p(assignment), use_w, _p(cut))

@@ -73,3 +73,23 @@ def test_round_half_even_target():
     _native.call("mp_initial_partition", 5, p(ip), p(ix), p(nw), 2, 5, p(a))
     assert np.array_equal(a, kway.initial_partition(ip, ix, nw, 2, 5))
     assert np.bincount(a).tolist() == [2, 3]  # round(2.5) == 2, not 3
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_rebalance_overloaded_random_assignments(seed):
+    """Unbalanced starting assignments (several over-cap blocks, some with no
+    room anywhere nearby): native rebalance == the reference restatement."""
+    ip, ix, w, rng = _graph(seed, n=int(np.random.default_rng(seed).integers(20, 240)))
+    n = len(ip) - 1
+    nw = rng.integers(1, 4, n).astype(np.int64)
+    nb = int(rng.integers(2, 12))
+    skew = rng.dirichlet(np.full(nb, 0.4))
+    a = rng.choice(nb, size=n, p=skew).astype(np.int64)
+    cap = int(max(1, nw.sum() // nb + rng.integers(-1, 4)))
+    for use_w in (1, 0):
+        a1, a2 = a.copy(), a.copy()
+        bw1 = np.bincount(a1, weights=nw, minlength=nb).astype(np.int64)
+        bw2 = bw1.copy()
+        _native.call("mp_rebalance", n, p(ip), p(ix), p(w), p(a1), p(bw1), nb, p(nw), cap, use_w)
+        kway.rebalance(ip, ix, w, a2, bw2, nw, cap, use_w)
+        assert np.array_equal(a1, a2) and np.array_equal(bw1, bw2)
