@@ -175,16 +175,25 @@ def partition_kway(g: ThreadGraph, cfg: PartitionConfig) -> Partition:
     def refine(ip, ix, w, a, nw):
         bw = np.bincount(a, weights=nw, minlength=nb).astype(np.int64)
         _native.call("mp_rebalance", len(nw), _p(ip), _p(ix), _p(w), _p(a), _p(bw), nb, _p(nw), cap, use_w)
+        # The reference asserts the cut never rises around each pass
+        # (partition.py:329-336).  A pass moves a node only for a strictly
+        # positive gain (numpy_impl.py:160-194: best_gain starts at 0, ties only
+        # between positive gains), and each move lowers the cut by its gain, so
+        # the assertion cannot fire; the two O(E) cut sweeps per pass are skipped
+        # (MESHPLAN_KWAY_CHECK=1 re-enables them).
+        check = bool(os.environ.get("MESHPLAN_KWAY_CHECK"))
         cut = np.zeros(1, dtype=np.int64)
         moves = np.zeros(1, dtype=np.int64)
         for _ in range(8):
-            _native.call("mp_cut_weight", len(nw), _p(ip), _p(ix), _p(w), _p(a), use_w, _p(cut))
-            before = int(cut[0])
+            if check:
+                _native.call("mp_cut_weight", len(nw), _p(ip), _p(ix), _p(w), _p(a), use_w, _p(cut))
+                before = int(cut[0])
             _native.call("mp_refine_boundary_pass", len(nw), _p(ip), _p(ix), _p(w), _p(a), _p(bw), nb, _p(nw), cap,
                          use_w, _p(moves))
-            _native.call("mp_cut_weight", len(nw), _p(ip), _p(ix), _p(w), _p(a), use_w, _p(cut))
-            if int(cut[0]) > before:
-                raise AssertionError(f"refinement increased cut: {before} -> {int(cut[0])}")
+            if check:
+                _native.call("mp_cut_weight", len(nw), _p(ip), _p(ix), _p(w), _p(a), use_w, _p(cut))
+                if int(cut[0]) > before:
+                    raise AssertionError(f"refinement increased cut: {before} -> {int(cut[0])}")
             if int(moves[0]) == 0:
                 break
 
