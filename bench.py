@@ -37,6 +37,7 @@ sys.path.insert(0, str(REPO))
 #: SURVEY 8d), the reference's k-way partition for the face loop (the config
 #: names k-way partitioned blocks; ~50 s to plan at 24M faces)
 DEFAULT_REORDER = {"C1": "gps", "C2": "gps", "C3": "none", "C4": "partition", "C5": "gps"}
+COMPARE_REORDER = {"C2": ("none", "gps")}
 CONFIGS = {
     # name: (family, dims, kernel, dtype, staging)
     "C1": ("quad2d", (848, 848), "flux", "f64", "all-indirect"),
@@ -321,6 +322,21 @@ def our_arm(args):
 
     if args.schedule == "best":
         args.schedule = min(SCHEDULES, key=lambda sc: statistics.median(results[f"hier_{sc}"]))
+    # the configs that compare block layouts (BASELINE.json configs[1]: natural
+    # vs GPS-reordered) time the other layout with the headline schedule too
+    vs_layout = {}
+    for other in COMPARE_REORDER.get(args.config, ()):
+        if other == args.reorder:
+            continue
+        t0 = time.perf_counter()
+        alt = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(
+            reorder=other, layout=args.layout, staging=staging, block_size=args.block_size))
+        t_alt = time.perf_counter() - t0
+        ms_alt = statistics.median(time_steps(mp.bind(alt, kernel, schedule=args.schedule).run, args.steps,
+                                              args.warmup, flush))
+        vs_layout[other] = {"ms_per_step": round(ms_alt, 5), "gbps": round(ub / (ms_alt * 1e-3) / 1e9, 2),
+                            "reuse_factor": round(mp.reuse_factor(alt), 4),
+                            "block_colours": alt.block_colours.num_colours, "plan_build_s": round(t_alt, 2)}
     # end to end through the public API with host buffers (pinned), H2D + D2H in the region
     main = loops[args.schedule]
     inputs = {a.array: hier.mesh.data[a.array].values for a in kernel.args}
@@ -369,6 +385,7 @@ def our_arm(args):
             "reuse_factor": round(mp.reuse_factor(hier), 4),
             "thread_colours_mean": round(float(hier.thread_colour_counts.mean()), 3),
         },
+        "vs_layout": vs_layout or None,
         "roofline": {"bound": "hbm", "achieved": round(gbps, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(gbps / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": f"{KERNEL_OF[args.schedule.split('-')[0]]} "
