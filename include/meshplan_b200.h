@@ -128,6 +128,7 @@ typedef struct mp_hier_plan {
   /* the same lists padded to 8 per ticket: -1 = no predecessor, -2 in slot 7 =
    * the list continues in tpreds (from its 8th entry) */
   const int32_t* tpred_pad;       /* [nb][8]                                 */
+  const int32_t* tblock_colour;   /* [nb] block id of each tdesc_colour entry */
 } mp_hier_plan;
 
 /* ---- library ------------------------------------------------------------ */

@@ -51,7 +51,7 @@ class MpHierPlan(ctypes.Structure):
         ("order", c_vp), ("pred_offsets", c_vp), ("preds", c_vp), ("flags", c_vp), ("tickets", c_vp),
         ("pull_off", c_vp), ("pull_ref", c_vp),
         ("tdesc_colour", c_vp), ("tdesc_order", c_vp), ("elem_meta", c_vp), ("elem_meta_bytes", c_i32),
-        ("pad2_", c_i32), ("tpred_offsets", c_vp), ("tpreds", c_vp), ("tpred_pad", c_vp),
+        ("pad2_", c_i32), ("tpred_offsets", c_vp), ("tpreds", c_vp), ("tpred_pad", c_vp), ("tblock_colour", c_vp),
     ]
 
 

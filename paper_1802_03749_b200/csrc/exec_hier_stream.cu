@@ -854,7 +854,7 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
     const int lo = P.colour_block_offsets_host[c], hi = P.colour_block_offsets_host[c + 1];
     if (hi <= lo) continue;
     H.tdesc = reinterpret_cast<const int4*>(P.tdesc_colour) + lo;
-    H.tblock = P.blocks_by_colour + lo;
+    H.tblock = P.tblock_colour + lo;
     H.ntickets = hi - lo;
     const int grid = (hi - lo) < resident ? (hi - lo) : resident;
     MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H, qmap));
@@ -872,7 +872,7 @@ mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool datafl
     if (s) return s;
     if (P.num_blocks == 0) return MP_OK;
     if (!P.written_is_staged) MP_FAIL(MP_ERR_KERNEL, "streamed executor needs written lists equal to staged lists");
-    if (!P.tdesc_colour || !P.tdesc_order || !P.elem_meta)
+    if (!P.tdesc_colour || !P.tdesc_order || !P.elem_meta || !P.tblock_colour)
       MP_FAIL(MP_ERR_KERNEL, "streamed executor needs the plan's ticket descriptors and element records");
     if (Op::ARITY > 8 || P.elem_meta_bytes < Op::ARITY * P.slot_bytes + 2 || P.elem_meta_bytes % 4)
       MP_FAIL(MP_ERR_KERNEL, "element records of %d bytes cannot hold %d slots, a colour and a first-writer mask", P.elem_meta_bytes,

@@ -25,6 +25,8 @@ Device tensors that the executors need stay resident in a ``DevicePlan``.
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import torch
 
@@ -309,6 +311,7 @@ class DevicePlan:
     tpred_off: torch.Tensor | None = None     # int32 [nb+1] predecessor CSR in ticket order
     tpreds: torch.Tensor | None = None        # int32 block ids
     tpred_pad: torch.Tensor | None = None     # int32 [nb][8] padded predecessor ids
+    tblock_colour: torch.Tensor | None = None  # int32 [nb] block of each tdesc_colour entry
 
     def finish_stream(self) -> None:
         """Streamed-executor structures: ticket descriptors {e0, k | nc << 16,
@@ -320,7 +323,9 @@ class DevicePlan:
         base = self.meta.clone()
         if nb:
             base[:, 1] |= self.colour_counts.to(torch.int32) << 16
-        self.tdesc_colour = base[self.blocks_by_colour.long()].contiguous() if nb else base
+        bbc = self.blocks_by_colour.long()
+        self.tdesc_colour = base[bbc].contiguous() if nb else base
+        self.tblock_colour = bbc.to(torch.int32).contiguous() if nb else self.blocks_by_colour
         self.tdesc_order = base[self.order.long()].contiguous() if nb else base
         # predecessor lists in ticket order (one indirection less for the sync warp)
         po = self.pred_off.long()
@@ -402,6 +407,7 @@ class DevicePlan:
         p.tpred_offsets = self.tpred_off.data_ptr()
         p.tpreds = self.tpreds.data_ptr()
         p.tpred_pad = self.tpred_pad.data_ptr()
+        p.tblock_colour = self.tblock_colour.data_ptr()
         return p
 
     def reschedule(self, lag: int) -> None:
