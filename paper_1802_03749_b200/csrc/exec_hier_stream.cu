@@ -738,10 +738,16 @@ inline int encode_row_map(CUtensorMap* map, const void* base, int esize, int dty
 }
 
 // Launch with programmatic stream serialization (PDL): consecutive colour
-// launches overlap one grid's tail with the next grid's prologue.
+// launches of one loop execution overlap one grid's tail with the next grid's
+// prologue, which gathers the loop's read-only data (read rows, direct
+// operands, plan records) before griddepcontrol.wait.  Only colour launches
+// after the first of a call use it: the first launch of a call may follow
+// any other work on the stream (e.g. a loop that writes this loop's read
+// array), so it is fully serialised.
 template <typename K, typename... Args>
-cudaError_t launch_pdl(K kern, int grid, int threads, size_t smem, cudaStream_t st, Args... args) {
+cudaError_t launch_pdl(K kern, int grid, int threads, size_t smem, cudaStream_t st, bool pdl, Args... args) {
   static const bool off = getenv("MESHPLAN_NO_PDL") != nullptr;
+  pdl = pdl && !off;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
@@ -749,7 +755,7 @@ cudaError_t launch_pdl(K kern, int grid, int threads, size_t smem, cudaStream_t 
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);
@@ -847,9 +853,10 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
     H.pred_pad = P.tpred_pad;
     H.ntickets = P.num_blocks;
     const int grid = P.num_blocks < resident ? P.num_blocks : resident;
-    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H, qmap));
+    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, false, v, H, qmap));
     return MP_OK;
   }
+  bool first = true;
   for (int c = 0; c < P.num_block_colours; ++c) {
     const int lo = P.colour_block_offsets_host[c], hi = P.colour_block_offsets_host[c + 1];
     if (hi <= lo) continue;
@@ -857,7 +864,8 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
     H.tblock = P.tblock_colour + lo;
     H.ntickets = hi - lo;
     const int grid = (hi - lo) < resident ? (hi - lo) : resident;
-    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, v, H, qmap));
+    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, !first, v, H, qmap));
+    first = false;
   }
   return MP_OK;
 }

@@ -361,3 +361,34 @@ def test_quad2d_structured_rejects_3d_shapes():
     kernel = mp.kernel_for_mesh("flux", mesh)
     with pytest.raises(mp.MeshValidationError):
         mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="structured:2,2,2"))
+
+
+def test_back_to_back_loops_reading_each_others_increments():
+    """Loop B reads (indirectly) the array loop A increments, launched back to
+    back on one stream: B must see A's complete result (the streamed
+    executor's programmatic-dependent launches never overlap across calls)."""
+    mesh = mp.generate_mesh("quad2d", (400, 360), dtype="f64")
+    kernel = mp.kernel_for_mesh("flux", mesh)
+    plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps"))
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n_q = plan.mesh.data["q"].values.size
+    n_w = plan.mesh.data["w"].values.size
+    X = torch.rand(n_q, generator=g, device="cuda", dtype=torch.float64)
+    W = torch.rand(n_w, generator=g, device="cuda", dtype=torch.float64)
+    for sched in ("stream", "stream-pull", "stream-dataflow"):
+        outs = []
+        for sync in (True, False):
+            Y = torch.zeros(n_q, device="cuda", dtype=torch.float64)
+            Z = torch.zeros(n_q, device="cuda", dtype=torch.float64)
+            a = mp.bind(plan, kernel, tensors={"q": X, "w": W, "res": Y}, schedule=sched)
+            b = mp.bind(plan, kernel, tensors={"q": Y, "w": W, "res": Z}, schedule=sched)
+            for _ in range(3):
+                a.run()
+                if sync:
+                    torch.cuda.synchronize()
+                b.run()
+                if sync:
+                    torch.cuda.synchronize()
+            torch.cuda.synchronize()
+            outs.append(Z.cpu().numpy())
+        assert bit_equal(outs[0], outs[1]), sched
