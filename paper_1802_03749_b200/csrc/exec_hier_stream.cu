@@ -917,7 +917,8 @@ extern "C" mp_status mp_exec_hier_stream(const mp_loop* loop, const mp_hier_plan
   if (!loop || !plan) MP_FAIL(MP_ERR_KERNEL, "null argument");
   const bool df = (schedule & 3) == MP_SCHED_DATAFLOW;
   const bool pull = !df && (schedule & MP_SCHED_PULL) != 0;
-  if (pull && (!plan->pull_off || !plan->pull_ref)) MP_FAIL(MP_ERR_KERNEL, "pull form needs the plan's pull lists");
+  if (pull && plan->num_blocks > 0 && (!plan->pull_off || !plan->pull_ref))
+    MP_FAIL(MP_ERR_KERNEL, "pull form needs the plan's pull lists");
   if (df && epoch == 0) MP_FAIL(MP_ERR_KERNEL, "dataflow epochs start at 1");
   cudaStream_t st = mp::as_stream(stream);
   const mp_loop& L = *loop;

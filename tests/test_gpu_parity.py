@@ -392,3 +392,31 @@ def test_back_to_back_loops_reading_each_others_increments():
             torch.cuda.synchronize()
             outs.append(Z.cpu().numpy())
         assert bit_equal(outs[0], outs[1]), sched
+
+
+@pytest.mark.parametrize("family,dims,kname", [
+    ("quad2d", (1, 1), "flux"), ("quad2d", (1, 2), "flux"), ("quad2d", (2, 1), "flux"), ("quad2d", (3, 3), "flux"),
+    ("tri2d", (1, 1), "flux"), ("hex3d-nodes", (1, 1, 1), "scatter8"), ("hex3d-faces", (1, 1, 1), "face-flux"),
+    ("hex3d-faces", (2, 1, 1), "face-flux"), ("hex3d-nodes", (2, 3, 1), "scatter8"),
+])
+def test_tiny_meshes_every_executor(family, dims, kname):
+    """Degenerate sizes (no elements, one element, one block smaller than a
+    warp): every strategy and schedule equals the oracle."""
+    from oracle import loops
+
+    mesh = mp.generate_mesh(family, dims, dtype="f64")
+    kernel = mp.kernel_for_mesh(kname, mesh)
+    inc = INC_OF[kname]
+    m = next(iter(mesh.mappings.values()))
+    read = {"flux": "q", "face-flux": "state"}.get(kname)
+    direct = {"flux": "w", "scatter8": "stress", "face-flux": "facew"}[kname]
+    want = loops.serial_loop(kname, m.table, None if read is None else mesh.data[read].view2d(),
+                             np.ascontiguousarray(mesh.data[direct].view2d()), _v2(mesh, inc))
+    assert bit_equal(_v2(mp.execute_serial(mesh, kernel), inc), want)
+    staging = "increment-only" if kname == "face-flux" else "all-indirect"
+    for strategy, reorder in (("global", "none"), ("global", "gps"), ("hier", "none"), ("hier", "gps")):
+        cfg = mp.PlanConfig(strategy=strategy, reorder=reorder, staging=staging, block_size=32)
+        plan = (mp.build_global_plan if strategy == "global" else mp.build_hierarchical_plan)(mesh, kernel, cfg)
+        for sched in (SCHEDULES if strategy == "hier" else ("-",)):
+            res, _ = _run(plan, kernel, sched)
+            assert bit_equal(_v2(plan.restore_data(res), inc), want), (strategy, reorder, sched)
