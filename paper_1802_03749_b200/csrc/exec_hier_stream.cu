@@ -60,7 +60,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "mp_loop.cuh"
 
@@ -837,11 +840,51 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   };
   // pull form: colour schedule only
   auto kern = dataflow ? pick_s(TT{}, FF{}) : (pull ? pick_s(FF{}, TT{}) : pick_s(FF{}, FF{}));
-  MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // attribute + occupancy queries cost microseconds of host time per call:
+  // cache them per (kernel, shared bytes, threads, device), process-wide
   int per_sm = 0, dev = 0, sms = 0;
-  MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   MP_CUDA_TRY(cudaGetDevice(&dev));
-  MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  {
+    struct Entry {
+      const void* k;
+      size_t smem;
+      int threads, dev, per_sm, sms;
+    };
+    struct Limit {
+      const void* k;
+      int dev;
+      size_t smem;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    static std::vector<Limit> limits;  // per (kernel, device): largest dynamic smem limit set
+    std::lock_guard<std::mutex> lock(mu);
+    const void* kp = reinterpret_cast<const void*>(kern);
+    Limit* lim = nullptr;
+    for (auto& e : limits)
+      if (e.k == kp && e.dev == dev) lim = &e;
+    if (!lim) {
+      limits.push_back({kp, dev, 0});
+      lim = &limits.back();
+    }
+    if (lim->smem < smem) {  // a larger limit stays valid for smaller launches
+      MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      lim->smem = smem;
+    }
+    bool hit = false;
+    for (const auto& e : cache)
+      if (e.k == kp && e.smem == smem && e.threads == threads && e.dev == dev) {
+        per_sm = e.per_sm;
+        sms = e.sms;
+        hit = true;
+        break;
+      }
+    if (!hit) {
+      MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+      MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      cache.push_back({kp, smem, threads, dev, per_sm, sms});
+    }
+  }
   if (per_sm < 1) MP_FAIL(MP_ERR_CAPACITY, "streamed executor does not fit on an SM (%zu shared bytes)", smem);
   if (env_ctas > 0 && env_ctas < per_sm) per_sm = env_ctas;
   const int resident = per_sm * sms;

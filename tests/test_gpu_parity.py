@@ -420,3 +420,21 @@ def test_tiny_meshes_every_executor(family, dims, kname):
         for sched in (SCHEDULES if strategy == "hier" else ("-",)):
             res, _ = _run(plan, kernel, sched)
             assert bit_equal(_v2(plan.restore_data(res), inc), want), (strategy, reorder, sched)
+
+
+@pytest.mark.parametrize("bs", [448, 480])
+def test_paper_block_sizes_every_schedule(bs):
+    """The paper's large blocks: every schedule exact vs
+    the oracle (the streamed executor's widest CTA is 480 + 32 threads)."""
+    from oracle import loops
+
+    mesh = mp.generate_mesh("quad2d", (120, 110), dtype="f64")
+    kernel = mp.kernel_for_mesh("flux", mesh)
+    m = mesh.mappings["e2c"]
+    want = loops.serial_loop("flux", m.table, mesh.data["q"].view2d(), np.ascontiguousarray(mesh.data["w"].view2d()),
+                             _v2(mesh, "res"))
+    for reorder in ("none", "gps", "partition"):
+        plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder=reorder, block_size=bs))
+        for sched in SCHEDULES:
+            res, _ = mp.execute_hierarchical(plan, kernel, schedule=sched)
+            assert bit_equal(_v2(plan.restore_data(res), "res"), want), (reorder, sched)
