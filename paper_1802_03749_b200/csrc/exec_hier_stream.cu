@@ -70,6 +70,9 @@
 #ifndef MP_STREAM_MAXREG
 #define MP_STREAM_MAXREG 72  // 7 CTAs of 128 threads per SM
 #endif
+#ifndef MP_STREAM_MAXREG_DF
+#define MP_STREAM_MAXREG_DF 64  // dataflow: 128 + 32 threads
+#endif
 
 namespace mp {
 namespace {
@@ -314,7 +317,7 @@ struct StreamLayout {
 };
 
 template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR, bool TMAQ, bool SR, bool PULL>
-__global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
+__global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
     hier_stream_kernel(LoopView<T> v, StreamView H, const __grid_constant__ CUtensorMap qmap) {
   constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
   using L_t = StreamLayout<Op, T>;
@@ -354,7 +357,6 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
     // the ready count is published) and the CTA's finished write-backs
     // (counted per warp in shared memory) into releases (before their flags).
     const int lane = tid & 31, fo = lane >> 3, slot = lane & 7;
-    const int nw = NT >> 5;
     int u = 0, released = 0, win = -1;
     int pid = -1;
     for (;;) {
@@ -370,7 +372,7 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
         for (int q = __ldg(H.pred_offsets + tk) + 7; q < q1; ++q)
           ok &= ld_relaxed_gpu(H.flags + __ldg(H.preds + q)) == H.epoch;
       }
-      const int done = ld_acquire_cta(ctl + 0) / nw;
+      const int done = ld_acquire_cta(ctl + 0);
       const unsigned bad = __ballot_sync(0xffffffffu, !ok);
       int nu = u + (bad ? (__ffs(bad) - 1) / 8 : 4);
       nu = nu < total ? nu : total;
@@ -565,6 +567,7 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
       qphase ^= 1u << s;
     }
     cbar();
+    if (DATAFLOW && t == 0) st_release_cta(ctl + 0, i);  // blocks < i are written back (this barrier)
     const unsigned char* st = smem + s * L.bytes;
     const int* hdr = reinterpret_cast<const int*>(st);
 
@@ -682,10 +685,6 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
       }
     }
     }  // push form
-    if constexpr (DATAFLOW) {  // this warp's write-back stores are done (release, CTA scope)
-      __syncwarp();
-      if ((t & 31) == 0) red_release_cta_add(ctl + 0, 1);
-    }
     // f. issue fill i+D into the stage block i-1 used (every thread passed
     //    this iteration's barrier after finishing block i-1); load block
     //    i+1's increment rows (its ids were stored by this thread)
@@ -699,6 +698,10 @@ __global__ void __maxnreg__(DATAFLOW ? 64 : MP_STREAM_MAXREG)
     s = s_next;
   }
   cp_wait(0);
+  if constexpr (DATAFLOW) {
+    named_sync(1, NT);
+    if (t == 0) st_release_cta(ctl + 0, total);
+  }
 }
 
 // ---- host: 2D row tensor maps for TMA gather4 ----
