@@ -71,7 +71,7 @@
 #define MP_STREAM_MAXREG 72  // 7 CTAs of 128 threads per SM
 #endif
 #ifndef MP_STREAM_MAXREG_DF
-#define MP_STREAM_MAXREG_DF 64  // dataflow: 128 + 32 threads
+#define MP_STREAM_MAXREG_DF 72  // dataflow: 128 + 32 threads, 5 CTAs/SM (64 spills on the critical path)
 #endif
 
 namespace mp {
