@@ -159,10 +159,13 @@ def partition_kway(g: ThreadGraph, cfg: PartitionConfig) -> Partition:
     tick = (lambda what: print(f"[kway] {what}: {time.perf_counter() - t0:.2f}s", flush=True)) if timing else (lambda what: None)
     while len(node_w) > target:
         visit = rng.permutation(len(node_w)).astype(np.int64)
+        tick(f"  visit order ({len(node_w)} nodes)")
         match = np.empty(len(node_w), dtype=np.int64)
         _native.call("mp_heavy_edge_matching", len(node_w), _p(indptr), _p(indices), _p(weights), _p(node_w),
                      _p(visit), max_cluster, _p(match))
+        tick("  matching")
         cip, cix, cw_e, cnw, cmap = _contract(indptr, indices, weights, node_w, match)
+        tick("  contraction")
         if len(cnw) >= 0.95 * len(node_w):
             break
         levels.append((indptr, indices, weights, node_w, cmap))
