@@ -319,6 +319,9 @@ def our_arm(args):
     t_plan_g = time.perf_counter() - t0
     gl = mp.bind(glob, kernel)
     results["global"] = time_steps(gl.run, args.steps, args.warmup, flush)
+    # atomics baseline (the paper's other race-avoidance strategy) on the same
+    # element order and layout as the hierarchical plan
+    results["atomic"] = time_steps(mp.bind(hier, kernel, schedule="atomic").run, args.steps, args.warmup, flush)
 
     if args.schedule == "best":
         args.schedule = min(SCHEDULES, key=lambda sc: statistics.median(results[f"hier_{sc}"]))
@@ -381,6 +384,8 @@ def our_arm(args):
             "global_reorder": args.global_reorder, "global_colours": glob.num_colours,
             "hier_ms_by_schedule": per_schedule,
             "speedup_hier_over_global": round(ms_glob / ms, 3),
+            "atomic_ms": round(statistics.median(results["atomic"]), 5),
+            "speedup_hier_over_atomic": round(statistics.median(results["atomic"]) / ms, 3),
             "block_colours": hier.block_colours.num_colours, "num_blocks": hier.num_blocks,
             "reuse_factor": round(mp.reuse_factor(hier), 4),
             "thread_colours_mean": round(float(hier.thread_colour_counts.mean()), 3),

@@ -169,6 +169,12 @@ mp_status mp_exec_hier_pipelined(const mp_loop* loop, const mp_hier_plan* plan, 
 mp_status mp_exec_hier_stream(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule, uint32_t epoch,
                               void* stream);
 
+/* Atomics baseline (reference cost model only,
+ * simulator.py:331-341): one thread per element in the loop's element order,
+ * increments applied with hardware atomics.  Results equal the reference up
+ * to floating-point reassociation.  A comparison baseline, not the product. */
+mp_status mp_exec_atomic(const mp_loop* loop, void* stream);
+
 /* execute_serial (simulator.py:215-230) on the device: per-element
  * increments to a temp array, then per point an ordered sum over its
  * (element, slot) references (inverse CSR, mesh.py:251-267), i.e. exactly the

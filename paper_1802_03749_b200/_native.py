@@ -63,6 +63,7 @@ _SIGNATURES = {
     "mp_exec_hier": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_u32, c_vp]),
     "mp_exec_hier_pipelined": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_u32, c_vp]),
     "mp_exec_hier_stream": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_u32, c_vp]),
+    "mp_exec_atomic": (c_i32, [ctypes.POINTER(MpLoop), c_vp]),
     "mp_exec_serial":(c_i32, [ctypes.POINTER(MpLoop), c_vp, c_vp, c_vp, c_vp]),
     "mp_race_check": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "mp_plan_block_points": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_i32, c_u32, c_i32, c_vp, c_vp, c_vp, c_vp]),

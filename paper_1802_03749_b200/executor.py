@@ -35,6 +35,8 @@ SCHEDULES = {
     "stream": (_native.MP_SCHED_COLOUR, "stream"),
     "stream-dataflow": (_native.MP_SCHED_DATAFLOW, "stream"),
     "stream-pull": (_native.MP_SCHED_COLOUR | _native.MP_SCHED_PULL, "stream"),
+    # comparison baseline (not bit-exact: atomics reassociate): ignores the colouring
+    "atomic": (_native.MP_SCHED_COLOUR, "atomic"),
 }
 TORCH_DTYPES = {"f64": torch.float64, "f32": torch.float32, "i64": torch.int64, "i32": torch.int32}
 
@@ -172,7 +174,9 @@ class DeviceLoop:
         """Launch one full execution of the loop (all colours); asynchronous."""
         sp = _native.stream_ptr(stream)
         dp = self.plan._device
-        if isinstance(self.plan, GlobalPlan):
+        if self.pipelined == "atomic":
+            _native.call("mp_exec_atomic", self.loop, sp)
+        elif isinstance(self.plan, GlobalPlan):
             offs = np.ascontiguousarray(dp.colour_offsets, dtype=np.int64)
             _native.call("mp_exec_global", self.loop, offs.ctypes.data, len(offs) - 1,
                          int(self.plan.config.block_size), sp)
@@ -211,6 +215,8 @@ class DeviceLoop:
         dst.copy_(self.tensors[inc].reshape(dst.shape), non_blocking=True)
 
     def launches_per_run(self) -> int:
+        if self.pipelined == "atomic":
+            return 1 if self.plan.mesh.sets[self.kernel.iter_set_name(self.plan.mesh)].size else 0
         if isinstance(self.plan, GlobalPlan):
             return int(np.count_nonzero(np.diff(self.plan._device.colour_offsets)))
         if self.schedule & 3 == _native.MP_SCHED_DATAFLOW:

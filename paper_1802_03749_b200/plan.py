@@ -230,8 +230,10 @@ def mesh_fingerprint(mesh: Mesh) -> dict:
     }
 
 
-def plan_to_dict(plan) -> dict:
+def plan_to_dict(plan, as_lists: bool = True) -> dict:
+    """The plan file content; arrays as lists (JSON) or numpy arrays (binary)."""
     c = plan.config
+    L = (lambda a: np.asarray(a).tolist()) if as_lists else (lambda a: np.asarray(a))  # noqa: E731
     out = {
         "format": PLAN_HEADER,
         "strategy": c.strategy,
@@ -239,47 +241,105 @@ def plan_to_dict(plan) -> dict:
                                                "epsilon", "seed", "unweighted_cut", "wide_transfers")},
         "hw": plan.hw.to_dict(),
         "kernel_key": plan.kernel_key,
-        "set_perms": {n: p.forward.tolist() for n, p in plan.set_perms.items() if not p.is_identity()},
+        "set_perms": {n: L(p.forward) for n, p in plan.set_perms.items() if not p.is_identity()},
         "array_layouts": dict(plan.array_layouts),
     }
     if isinstance(plan, GlobalPlan):
-        out["global"] = {"colours": plan.colours.colours.tolist(), "num_colours": plan.colours.num_colours,
-                         "colour_offsets": plan.colour_offsets.tolist()}
+        out["global"] = {"colours": L(plan.colours.colours), "num_colours": plan.colours.num_colours,
+                         "colour_offsets": L(plan.colour_offsets)}
         return out
 
     def csr(d):
-        return {k: {"indptr": v[0].tolist(), "ids": v[1].tolist()} for k, v in d.items()}
+        return {k: {"indptr": L(v[0]), "ids": L(v[1])} for k, v in d.items()}
 
     out["hier"] = {
-        "block_offsets": plan.block_offsets.tolist(),
-        "block_colours": plan.block_colours.colours.tolist(),
+        "block_offsets": L(plan.block_offsets),
+        "block_colours": L(plan.block_colours.colours),
         "num_block_colours": plan.block_colours.num_colours,
-        "thread_colours": plan.thread_colours.tolist(),
-        "thread_colour_counts": plan.thread_colour_counts.tolist(),
+        "thread_colours": L(plan.thread_colours),
+        "thread_colour_counts": L(plan.thread_colour_counts),
         "staged": csr(plan.staged),
         "written": csr(plan.written),
-        "shared_bytes": plan.shared_bytes.tolist(),
+        "shared_bytes": L(plan.shared_bytes),
         "refs_per_element": plan.refs_per_element,
         "partition_meta": plan.partition_meta,
     }
     return out
 
 
-def save_plan(plan, path, mesh: Mesh | None = None) -> None:
-    data = plan_to_dict(plan)
+# Binary plan files (extension): the same content as the
+# JSON format with every array stored raw in an uncompressed .npz (C5 plans
+# are ~1.5 GB as JSON text).  The header is the JSON dict with each array
+# replaced by a reference into the archive.
+_NPZ_REF = "__npz__"
+
+
+def _to_binary(data: dict, arrays: dict, prefix: str = "") -> dict:
+    out = {}
+    for k, v in data.items():
+        key = f"{prefix}{k}"
+        if isinstance(v, dict):
+            out[k] = _to_binary(v, arrays, key + "/")
+        elif isinstance(v, np.ndarray):
+            a = v.astype(np.int32) if v.dtype == np.int64 and (v.size == 0 or (v.min() >= -2**31 and v.max() < 2**31)) else v
+            arrays[key] = np.ascontiguousarray(a)
+            out[k] = {_NPZ_REF: key, "dtype": str(v.dtype)}
+        else:
+            out[k] = v
+    return out
+
+
+def _from_binary(data: dict, arrays) -> dict:
+    out = {}
+    for k, v in data.items():
+        if isinstance(v, dict) and _NPZ_REF in v:
+            out[k] = np.asarray(arrays[v[_NPZ_REF]]).astype(v["dtype"])
+        elif isinstance(v, dict):
+            out[k] = _from_binary(v, arrays)
+        else:
+            out[k] = v
+    return out
+
+
+def save_plan(plan, path, mesh: Mesh | None = None, binary: bool | None = None) -> None:
+    """Write a plan file: the reference's JSON format (plan.py:619-755), or the
+    binary .npz form when ``binary`` (default: the path ends with .npz)."""
+    binary = str(path).endswith(".npz") if binary is None else binary
+    data = plan_to_dict(plan, as_lists=not binary)
     if mesh is not None:
         data["mesh_fingerprint"] = mesh_fingerprint(mesh)
+    if binary:
+        arrays = {}
+        header = _to_binary(data, arrays)
+        arrays["__header__"] = np.frombuffer(json.dumps(header, sort_keys=True).encode(), dtype=np.uint8)
+        with open(path, "wb") as fh:
+            np.savez(fh, **arrays)
+        return
     with open(path, "w", encoding="utf-8") as fh:
         json.dump(data, fh, sort_keys=True, separators=(",", ":"))
         fh.write("\n")
 
 
 def load_plan(path, mesh: Mesh):
+    with open(path, "rb") as fh:
+        magic = fh.read(2)
+    if magic == b"PK":  # binary plan (.npz)
+        try:
+            with np.load(path, allow_pickle=False) as z:
+                header = json.loads(bytes(z["__header__"]).decode())
+                data = _from_binary(header, z)
+        except (ValueError, KeyError, OSError) as exc:
+            raise FileFormatError(f"{path}: bad binary plan: {exc}") from None
+        return _plan_from_dict(data, mesh, path)
     with open(path, "r", encoding="utf-8") as fh:
         try:
             data = json.load(fh)
         except ValueError as exc:
             raise FileFormatError(f"{path}: bad plan JSON: {exc}") from None
+    return _plan_from_dict(data, mesh, path)
+
+
+def _plan_from_dict(data: dict, mesh: Mesh, path):
     if data.get("format") != PLAN_HEADER:
         raise FileFormatError(f"{path}: not a meshplan plan file")
     fp = data.get("mesh_fingerprint")

@@ -438,3 +438,28 @@ def test_paper_block_sizes_every_schedule(bs):
         for sched in SCHEDULES:
             res, _ = mp.execute_hierarchical(plan, kernel, schedule=sched)
             assert bit_equal(_v2(plan.restore_data(res), "res"), want), (reorder, sched)
+
+
+@pytest.mark.parametrize("family,dims,kname", [("quad2d", (64, 48), "flux"), ("hex3d-nodes", (10, 9, 8), "scatter8"),
+                                               ("hex3d-faces", (9, 8, 7), "face-flux")])
+def test_atomic_baseline_exact_on_grid_data(family, dims, kname):
+    """Atomics baseline: reassociated sums, exact on the generators' 1/1024
+    grid data (every partial sum is representable)."""
+    from oracle import loops
+
+    mesh = mp.generate_mesh(family, dims, dtype="f64")
+    kernel = mp.kernel_for_mesh(kname, mesh)
+    inc = INC_OF[kname]
+    m = next(iter(mesh.mappings.values()))
+    read = {"flux": "q", "face-flux": "state"}.get(kname)
+    direct = {"flux": "w", "scatter8": "stress", "face-flux": "facew"}[kname]
+    want = loops.serial_loop(kname, m.table, None if read is None else mesh.data[read].view2d(),
+                             np.ascontiguousarray(mesh.data[direct].view2d()), _v2(mesh, inc))
+    staging = "increment-only" if kname == "face-flux" else "all-indirect"
+    plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps", staging=staging))
+    lp = mp.bind(plan, kernel, schedule="atomic")
+    lp.run()
+    torch.cuda.synchronize()
+    arr = plan.mesh.data[inc]
+    res = plan.mesh.with_data(mp.DataArray(arr.name, arr.set, arr.components, lp.tensors[inc].cpu().numpy(), arr.layout))
+    assert np.array_equal(_v2(plan.restore_data(res), inc), want)
