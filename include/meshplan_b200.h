@@ -246,11 +246,26 @@ mp_status mp_cut_weight(int64_t n, const int64_t* indptr, const int64_t* indices
 mp_status mp_refine_boundary_pass(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
                                   int64_t* assignment, int64_t* block_w, int64_t num_blocks, const int64_t* node_w,
                                   int64_t cap, int32_t use_w, int64_t* moves);
+/* Up to `max_passes` of those sweeps, stopping after one with no move
+ * (partition.py:326-337); later sweeps visit only the nodes whose decision can
+ * change.  `moves` receives the total over all sweeps. */
+mp_status mp_refine_boundary(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
+                             int64_t* assignment, int64_t* block_w, int64_t num_blocks, const int64_t* node_w,
+                             int64_t cap, int32_t use_w, int32_t max_passes, int64_t* moves);
 mp_status mp_rebalance(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* weights,
                        int64_t* assignment, int64_t* block_w, int64_t num_blocks, const int64_t* node_w, int64_t cap,
                        int32_t use_w);
 mp_status mp_initial_partition(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* node_w,
                                int64_t num_blocks, int64_t cap, int64_t* assignment);
+
+/* mp_heavy_edge_matching on device arrays (numpy_impl.py:134-157; replaces
+ * _accel.heavy_edge_matching at partition.py:317): the same matching as the
+ * sequential visit-order greedy, computed in dependency rounds (a node acts
+ * once every earlier-visited node within two hops is matched).  `rounds`
+ * receives the number of rounds. */
+mp_status mp_heavy_edge_matching_device(int32_t n, const int64_t* indptr, const int64_t* indices,
+                                        const int64_t* weights, const int64_t* node_w, const int64_t* visit,
+                                        int64_t max_cluster, int64_t* match, int32_t* rounds, void* stream);
 
 /* Level-synchronous BFS on a device CSR graph (numpy_impl.py:114-131):
  * levels[v] (-1 unreached); returns the eccentricity and visited count.

@@ -77,6 +77,8 @@ _SIGNATURES = {
     "mp_heavy_edge_matching": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "mp_cut_weight": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "mp_refine_boundary_pass": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_vp]),
+    "mp_heavy_edge_matching_device": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "mp_refine_boundary": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_vp]),
     "mp_rebalance": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32]),
     "mp_initial_partition": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]),
     "mp_halo_pack":(c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),

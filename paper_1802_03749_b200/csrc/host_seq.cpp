@@ -14,6 +14,7 @@
 #include <cmath>
 #include <limits>
 #include <set>
+#include <thread>
 #include <utility>
 #include <vector>
 #include <cstdint>
@@ -239,6 +240,112 @@ extern "C" mp_status mp_refine_boundary_pass(int64_t n, const int64_t* indptr, c
     for (int64_t k = 0; k < nt; ++k) conn[touched[k]] = 0;
   }
   *moves_out = moves;
+  return MP_OK;
+}
+
+// partition.py:326-337 -- up to `max_passes` boundary sweeps (stopping after a
+// sweep with no move), the same decisions as repeated mp_refine_boundary_pass
+// calls but with every sweep after the first visiting only the nodes whose
+// decision can differ.  A node can move only if some neighbouring block beats
+// its own block's connectivity (a positive-gain candidate); whether it has one
+// depends only on its neighbours' blocks.  So a node that last saw no such
+// candidate keeps that outcome until a neighbour moves, and a node that had
+// one but was blocked by the weight cap is re-checked every sweep.  Visited in
+// ascending order (the reference's order) with the flags maintained as moves
+// happen: a move flags the mover and all its neighbours for the next sweep,
+// and its later-ordered neighbours for the current one.  For large graphs the
+// first sweep's flags come from a multi-threaded scan of the starting state.
+extern "C" mp_status mp_refine_boundary(int64_t n, const int64_t* indptr, const int64_t* indices,
+                                        const int64_t* weights, int64_t* assignment, int64_t* block_w,
+                                        int64_t num_blocks, const int64_t* node_w, int64_t cap, int32_t use_w,
+                                        int32_t max_passes, int64_t* moves_out) {
+  mp::clear_error();
+  const int64_t nbk = num_blocks > 0 ? num_blocks : 1, nwords = (n + 63) / 64;
+  std::vector<int64_t> conn(nbk, 0), touched(nbk);
+  // flag bitsets: a sweep clears the bits it visits, so both are all-zero
+  // again when it ends and need no O(n) reset
+  std::vector<uint64_t> cur(nwords, ~0ull), nxt(nwords, 0);
+  if (n % 64) cur[nwords - 1] = (1ull << (n % 64)) - 1;
+  // Positive-gain test for the first sweep's flags (multi-threaded, each
+  // thread owning whole words of the bitset).
+  auto positive_at = [&](int64_t u, int64_t* c, int64_t* tch) {
+    const int64_t own = assignment[u];
+    int64_t nt = 0;
+    for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) {
+      const int64_t b = assignment[indices[j]];
+      if (c[b] == 0) tch[nt++] = b;
+      c[b] += use_w ? weights[j] : 1;
+    }
+    bool positive = false;
+    for (int64_t k = 0; k < nt; ++k) positive |= tch[k] != own && c[tch[k]] > c[own];
+    for (int64_t k = 0; k < nt; ++k) c[tch[k]] = 0;
+    return positive;
+  };
+  if (n >= (1 << 16) && max_passes > 0) {
+    const int nth = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nth; ++t)
+      pool.emplace_back([&, t]() {
+        std::vector<int64_t> c(nbk, 0), tch(nbk);
+        for (int64_t wi = nwords * t / nth; wi < nwords * (t + 1) / nth; ++wi) {
+          uint64_t bits = 0;
+          for (int64_t u = wi * 64; u < std::min(n, wi * 64 + 64); ++u)
+            if (positive_at(u, c.data(), tch.data())) bits |= 1ull << (u - wi * 64);
+          cur[wi] = bits;
+        }
+      });
+    for (auto& th : pool) th.join();
+  }
+  int64_t total = 0;
+  for (int pass = 0; pass < max_passes; ++pass) {
+    int64_t moves = 0;
+    for (int64_t wi = 0; wi < nwords; ++wi) {
+      while (uint64_t bits = cur[wi]) {  // re-read: a move may flag later nodes of this word
+        cur[wi] = bits & (bits - 1);
+        const int64_t u = wi * 64 + __builtin_ctzll(bits);
+        const int64_t own = assignment[u];
+        int64_t nt = 0;
+        for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) {
+          const int64_t b = assignment[indices[j]];
+          if (conn[b] == 0) touched[nt++] = b;
+          conn[b] += use_w ? weights[j] : 1;
+        }
+        int64_t best = own, best_gain = 0;
+        bool positive = false;
+        for (int64_t k = 0; k < nt; ++k) {
+          const int64_t b = touched[k];
+          if (b == own) continue;
+          const int64_t gain = conn[b] - conn[own];
+          positive |= gain > 0;
+          if (gain > best_gain || (gain == best_gain && best != own && b < best)) {
+            if (block_w[b] + node_w[u] <= cap && block_w[own] - node_w[u] > 0) {
+              best = b;
+              best_gain = gain;
+            }
+          }
+        }
+        for (int64_t k = 0; k < nt; ++k) conn[touched[k]] = 0;
+        if (best != own) {
+          assignment[u] = best;
+          block_w[own] -= node_w[u];
+          block_w[best] += node_w[u];
+          ++moves;
+          nxt[u >> 6] |= 1ull << (u & 63);
+          for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) {
+            const int64_t v = indices[j];
+            nxt[v >> 6] |= 1ull << (v & 63);
+            if (v > u) cur[v >> 6] |= 1ull << (v & 63);
+          }
+        } else if (positive) {
+          nxt[u >> 6] |= 1ull << (u & 63);
+        }
+      }
+    }
+    total += moves;
+    cur.swap(nxt);
+    if (moves == 0) break;
+  }
+  *moves_out = total;
   return MP_OK;
 }
 

@@ -3,6 +3,8 @@
 //   * block conflict DAG + topological schedule for the dataflow executor
 //   * level-synchronous BFS (numpy_impl.py:114-131; levels are visit-order
 //     independent, so GPS levels equal the reference's)
+//   * heavy-edge matching (numpy_impl.py:134-157) in dependency rounds, equal
+//     to the reference's sequential visit-order greedy
 #include <cub/cub.cuh>
 #include <limits.h>
 
@@ -173,6 +175,85 @@ inline int grid_for(int64_t n, int threads = 256) {
   if (g < 1) g = 1;
   if (g > 148 * 32) g = 148 * 32;
   return (int)g;
+}
+
+
+// ---- heavy-edge matching ------------------------------------------------------------
+// The reference visits nodes in a random order; an unmatched node takes its
+// heaviest available neighbour (ties: lowest id).  Node u's turn reads only
+// the matched state of its neighbours, which the earlier turns of nodes within
+// two hops decide.  So u can act as soon as every earlier-ranked node within
+// two hops of it has been matched: all such "ready" nodes act together on the
+// previous round's state (two ready nodes are more than two hops apart, so
+// they never pick the same partner or each other), and the result is the
+// sequential one.  The earliest unmatched node is always ready.
+__global__ void hem_rank_kernel(int32_t n, const int64_t* __restrict__ visit, int32_t* rank, int32_t* work,
+                                int64_t* match) {
+  for (int32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    rank[visit[s]] = s;
+    work[s] = s;
+    match[s] = -1;
+  }
+}
+
+__global__ void hem_round_kernel(int32_t m, const int32_t* __restrict__ work, const int64_t* __restrict__ indptr,
+                                 const int64_t* __restrict__ indices, const int64_t* __restrict__ weights,
+                                 const int64_t* __restrict__ node_w, const int32_t* __restrict__ rank,
+                                 int64_t max_cluster, const int64_t* __restrict__ match, int64_t* __restrict__ dec) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int64_t u = work[i];
+    if (match[u] >= 0) {  // taken as a partner last round
+      dec[i] = -3;
+      continue;
+    }
+    const int32_t r = rank[u];
+    const int64_t a = indptr[u], z = indptr[u + 1];
+    bool ready = true;
+    for (int64_t j = a; j < z && ready; ++j) {
+      const int64_t v = indices[j];
+      if (v == u || match[v] >= 0) continue;  // a matched neighbour stays unavailable
+      if (rank[v] < r) {
+        ready = false;
+        break;
+      }
+      for (int64_t k = indptr[v]; k < indptr[v + 1]; ++k) {
+        const int64_t x = indices[k];
+        if (x != u && rank[x] < r && match[x] < 0) {
+          ready = false;
+          break;
+        }
+      }
+    }
+    if (!ready) {
+      dec[i] = -2;
+      continue;
+    }
+    int64_t best = u, best_w = -1;
+    for (int64_t j = a; j < z; ++j) {
+      const int64_t v = indices[j];
+      if (match[v] >= 0 || v == u) continue;
+      if (node_w[u] + node_w[v] > max_cluster) continue;
+      const int64_t w = weights[j];
+      if (w > best_w || (w == best_w && v < best)) {
+        best = v;
+        best_w = w;
+      }
+    }
+    dec[i] = best;
+  }
+}
+
+__global__ void hem_apply_kernel(int32_t m, const int32_t* __restrict__ work, const int64_t* __restrict__ dec,
+                                 int64_t* match, int32_t* next, int32_t* count) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int64_t u = work[i], d = dec[i];
+    if (d >= 0) {
+      match[u] = d;
+      if (d != u) match[d] = u;
+    } else if (d == -2) {
+      next[atomicAdd(count, 1)] = (int32_t)u;
+    }
+  }
 }
 
 }  // namespace
@@ -362,5 +443,44 @@ extern "C" mp_status mp_bfs_levels(int32_t n, const int64_t* indptr, const int32
   MP_CUDA_TRY(ce);
   *ecc = level;
   *visited = total;
+  return MP_OK;
+}
+
+extern "C" mp_status mp_heavy_edge_matching_device(int32_t n, const int64_t* indptr, const int64_t* indices,
+                                                   const int64_t* weights, const int64_t* node_w,
+                                                   const int64_t* visit, int64_t max_cluster, int64_t* match,
+                                                   int32_t* rounds, void* stream) {
+  clear_error();
+  *rounds = 0;
+  if (n < 0) MP_FAIL(MP_ERR_VALIDATION, "negative node count");
+  if (n == 0) return MP_OK;
+  cudaStream_t st = as_stream(stream);
+  Scratch rk(st), wa(st), wb(st), dec(st), cnt(st);
+  MP_CUDA_TRY(rk.alloc((size_t)n * 4));
+  MP_CUDA_TRY(wa.alloc((size_t)n * 4));
+  MP_CUDA_TRY(wb.alloc((size_t)n * 4));
+  MP_CUDA_TRY(dec.alloc((size_t)n * 8));
+  MP_CUDA_TRY(cnt.alloc(4));
+  int32_t* pinned = nullptr;
+  MP_CUDA_TRY(cudaMallocHost(&pinned, 4));
+  hem_rank_kernel<<<grid_for(n), 256, 0, st>>>(n, visit, rk.as<int32_t>(), wa.as<int32_t>(), match);
+  cudaError_t ce = cudaGetLastError();
+  int32_t m = n, r = 0;
+  int32_t *cur = wa.as<int32_t>(), *nxt = wb.as<int32_t>();
+  while (ce == cudaSuccess && m > 0) {
+    if ((ce = cudaMemsetAsync(cnt.p, 0, 4, st))) break;
+    hem_round_kernel<<<grid_for(m), 256, 0, st>>>(m, cur, indptr, indices, weights, node_w, rk.as<int32_t>(),
+                                                  max_cluster, match, dec.as<int64_t>());
+    hem_apply_kernel<<<grid_for(m), 256, 0, st>>>(m, cur, dec.as<int64_t>(), match, nxt, cnt.as<int32_t>());
+    if ((ce = cudaGetLastError())) break;
+    if ((ce = cudaMemcpyAsync(pinned, cnt.p, 4, cudaMemcpyDeviceToHost, st))) break;
+    if ((ce = cudaStreamSynchronize(st))) break;
+    m = *pinned;
+    ++r;
+    std::swap(cur, nxt);
+  }
+  cudaFreeHost(pinned);
+  MP_CUDA_TRY(ce);
+  *rounds = r;
   return MP_OK;
 }

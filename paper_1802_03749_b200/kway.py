@@ -6,8 +6,10 @@ and its point reordering (reorder.py:174-203):
 * thread graph G_M (elements adjacent when they share a point, weight =
   distinct shared points) -- GPU (sort / unique / segment pairs);
 * coarsening: the reference's numpy PCG64 visit orders (drawn here with the
-  same ``np.random.default_rng(seed)`` calls, level by level), native
-  heavy-edge matching, contraction on the GPU;
+  same ``np.random.default_rng(seed)`` calls, level by level), heavy-edge
+  matching and contraction on the GPU (the matching in dependency rounds that
+  reproduce the sequential greedy; MESHPLAN_HOST_MATCHING=1 runs the native
+  host sweep instead);
 * recursive region-growing bisection, rebalancing and boundary-refinement
   sweeps -- native host C++ (inherently sequential, in-place sweeps);
 * writer-set point order -- GPU stable LSD sorts over padded block tuples.
@@ -16,7 +18,7 @@ and its point reordering (reorder.py:174-203):
 import math
 import os
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -32,6 +34,7 @@ class ThreadGraph:
     indptr: np.ndarray
     indices: np.ndarray
     weights: np.ndarray
+    device: tuple = field(default=None, compare=False, repr=False)  # device (indptr, indices, weights), if built there
 
     @property
     def num_edges(self) -> int:
@@ -103,11 +106,10 @@ def build_thread_graph(mappings) -> ThreadGraph:
     return ThreadGraph(m.from_set.size, ip.cpu().numpy(), ix.cpu().numpy(), w.cpu().numpy())
 
 
-def _contract(indptr, indices, weights, node_w, match):
-    """partition._contract (173-195) on the GPU; returns host int64 arrays."""
-    dev = "cuda"
-    t = lambda a: torch.as_tensor(a, device=dev)  # noqa: E731
-    ip, ix, ew, nw, mt = t(indptr), t(indices), t(weights), t(node_w), t(match)
+def _contract(ip, ix, ew, nw, mt):
+    """partition._contract (173-195) on device tensors; returns device tensors
+    (indptr, indices, weights, node_w, cmap) of the coarse graph."""
+    dev = ip.device
     n = nw.numel()
     rep = torch.minimum(torch.arange(n, device=dev), mt)
     reps = torch.unique(rep)
@@ -127,8 +129,20 @@ def _contract(indptr, indices, weights, node_w, match):
     cip = torch.zeros(nc + 1, dtype=torch.long, device=dev)
     if r.numel():
         cip[1:] = torch.cumsum(torch.bincount(r, minlength=nc), 0)
-    h = lambda x: x.cpu().numpy().astype(np.int64)  # noqa: E731
-    return h(cip), h(c), h(summed), h(cw), h(cmap)
+    return cip, c, summed, cw, cmap
+
+
+def _match_device(ip, ix, ew, nw, visit: np.ndarray, max_cluster: int) -> torch.Tensor:
+    """_accel.heavy_edge_matching (partition.py:317) on the GPU, in dependency
+    rounds (mp_heavy_edge_matching_device); equal to the sequential greedy."""
+    n = nw.numel()
+    vis = torch.as_tensor(visit, device=ip.device)
+    match = torch.empty(n, dtype=torch.long, device=ip.device)
+    rounds = np.zeros(1, dtype=np.int32)
+    _native.call("mp_heavy_edge_matching_device", n, _native.ptr(ip), _native.ptr(ix), _native.ptr(ew),
+                 _native.ptr(nw), _native.ptr(vis), int(max_cluster), _native.ptr(match), rounds.ctypes.data,
+                 torch.cuda.current_stream().cuda_stream)
+    return match
 
 
 def _p(a: np.ndarray) -> int:
@@ -157,19 +171,31 @@ def partition_kway(g: ThreadGraph, cfg: PartitionConfig) -> Partition:
     timing = os.environ.get("MESHPLAN_KWAY_TIMING")
     t0 = time.perf_counter()
     tick = (lambda what: print(f"[kway] {what}: {time.perf_counter() - t0:.2f}s", flush=True)) if timing else (lambda what: None)
+    host_match = bool(os.environ.get("MESHPLAN_HOST_MATCHING"))
+    h = lambda x: x.cpu().numpy().astype(np.int64)  # noqa: E731
+    if g.device is not None:
+        gd = tuple(t.long() for t in g.device)
+    else:
+        gd = tuple(torch.as_tensor(a, device="cuda") for a in (indptr, indices, weights))
+    nw_d = torch.ones(n, dtype=torch.long, device=gd[0].device)
     while len(node_w) > target:
         visit = rng.permutation(len(node_w)).astype(np.int64)
         tick(f"  visit order ({len(node_w)} nodes)")
-        match = np.empty(len(node_w), dtype=np.int64)
-        _native.call("mp_heavy_edge_matching", len(node_w), _p(indptr), _p(indices), _p(weights), _p(node_w),
-                     _p(visit), max_cluster, _p(match))
+        if host_match:
+            match = np.empty(len(node_w), dtype=np.int64)
+            _native.call("mp_heavy_edge_matching", len(node_w), _p(indptr), _p(indices), _p(weights), _p(node_w),
+                         _p(visit), max_cluster, _p(match))
+            match_d = torch.as_tensor(match, device=gd[0].device)
+        else:
+            match_d = _match_device(*gd, nw_d, visit, max_cluster)
         tick("  matching")
-        cip, cix, cw_e, cnw, cmap = _contract(indptr, indices, weights, node_w, match)
+        cip_d, cix_d, cw_d, cnw_d, cmap_d = _contract(*gd, nw_d, match_d)
         tick("  contraction")
-        if len(cnw) >= 0.95 * len(node_w):
+        if cnw_d.numel() >= 0.95 * len(node_w):
             break
-        levels.append((indptr, indices, weights, node_w, cmap))
-        indptr, indices, weights, node_w = cip, cix, cw_e, cnw
+        levels.append((indptr, indices, weights, node_w, h(cmap_d)))
+        gd, nw_d = (cip_d, cix_d, cw_d), cnw_d
+        indptr, indices, weights, node_w = h(cip_d), h(cix_d), h(cw_d), h(cnw_d)
     tick(f"coarsening ({len(levels)} levels, coarsest {len(node_w)} nodes)")
     assignment = np.empty(len(node_w), dtype=np.int64)
     _native.call("mp_initial_partition", len(node_w), _p(indptr), _p(indices), _p(node_w), nb, cap, _p(assignment))
@@ -178,6 +204,7 @@ def partition_kway(g: ThreadGraph, cfg: PartitionConfig) -> Partition:
     def refine(ip, ix, w, a, nw):
         bw = np.bincount(a, weights=nw, minlength=nb).astype(np.int64)
         _native.call("mp_rebalance", len(nw), _p(ip), _p(ix), _p(w), _p(a), _p(bw), nb, _p(nw), cap, use_w)
+        tick("    rebalance")
         # The reference asserts the cut never rises around each pass
         # (partition.py:329-336).  A pass moves a node only for a strictly
         # positive gain (numpy_impl.py:160-194: best_gain starts at 0, ties only
@@ -187,6 +214,10 @@ def partition_kway(g: ThreadGraph, cfg: PartitionConfig) -> Partition:
         check = bool(os.environ.get("MESHPLAN_KWAY_CHECK"))
         cut = np.zeros(1, dtype=np.int64)
         moves = np.zeros(1, dtype=np.int64)
+        if not check:  # the 8 sweeps in one call, later sweeps over the changed frontier only
+            _native.call("mp_refine_boundary", len(nw), _p(ip), _p(ix), _p(w), _p(a), _p(bw), nb, _p(nw), cap,
+                         use_w, 8, _p(moves))
+            return
         for _ in range(8):
             if check:
                 _native.call("mp_cut_weight", len(nw), _p(ip), _p(ix), _p(w), _p(a), use_w, _p(cut))
@@ -204,6 +235,7 @@ def partition_kway(g: ThreadGraph, cfg: PartitionConfig) -> Partition:
     tick("refine coarsest")
     for fip, fix, fw, fnw, cmap in reversed(levels):
         assignment = np.ascontiguousarray(assignment[cmap])
+        tick("    projection")
         indptr, indices, weights, node_w = fip, fix, fw, fnw
         refine(indptr, indices, weights, assignment, node_w)
         tick(f"refine level with {len(fnw)} nodes")
@@ -258,7 +290,7 @@ def partition_for_plan(map_d: torch.Tensor, npts: int, config) -> PlanPartition:
     """The partition branch of plan._reorder_for_plan (plan.py:330-352)."""
     n = map_d.shape[0]
     ip, ix, w = thread_graph_device(map_d, npts)
-    g = ThreadGraph(n, ip.cpu().numpy(), ix.cpu().numpy(), w.cpu().numpy())
+    g = ThreadGraph(n, ip.cpu().numpy(), ix.cpu().numpy(), w.cpu().numpy(), device=(ip, ix, w))
     part = partition_kway(g, config.partition_config())
     a = torch.as_tensor(part.assignment, device=map_d.device)
     order = torch.as_tensor(np.argsort(part.assignment, kind="stable"), device=map_d.device)

@@ -93,3 +93,66 @@ def test_rebalance_overloaded_random_assignments(seed):
         _native.call("mp_rebalance", n, p(ip), p(ix), p(w), p(a1), p(bw1), nb, p(nw), cap, use_w)
         kway.rebalance(ip, ix, w, a2, bw2, nw, cap, use_w)
         assert np.array_equal(a1, a2) and np.array_equal(bw1, bw2)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_refine_boundary_frontier_equals_repeated_passes(seed):
+    """mp_refine_boundary (frontier-only later sweeps) == up to 8 full
+    reference sweeps (partition.py:329-338) from skewed random assignments."""
+    ip, ix, w, rng = _graph(seed, n=int(np.random.default_rng(seed + 100).integers(20, 300)))
+    n = len(ip) - 1
+    nw = rng.integers(1, 3, n).astype(np.int64)
+    nb = int(rng.integers(2, 10))
+    a = rng.choice(nb, size=n, p=rng.dirichlet(np.full(nb, 2.0))).astype(np.int64)
+    cap = int(max(1, nw.sum() // nb + rng.integers(0, 6)))
+    for use_w in (1, 0):
+        a1, a2 = a.copy(), a.copy()
+        bw1 = np.bincount(a1, weights=nw, minlength=nb).astype(np.int64)
+        bw2 = bw1.copy()
+        total = 0
+        for _ in range(8):
+            m = kway.refine_boundary_pass(ip, ix, w, a2, bw2, nw, cap, use_w)
+            total += m
+            if m == 0:
+                break
+        moves = np.zeros(1, dtype=np.int64)
+        _native.call("mp_refine_boundary", n, p(ip), p(ix), p(w), p(a1), p(bw1), nb, p(nw), cap, use_w, 8, p(moves))
+        assert np.array_equal(a1, a2) and np.array_equal(bw1, bw2) and int(moves[0]) == total
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_refine_boundary_threaded_first_sweep(seed):
+    """Graphs above the threaded pre-scan threshold (2^16 nodes): the same
+    result as repeated full single sweeps (each checked against the oracle
+    above)."""
+    rng = np.random.default_rng(seed)
+    side = 300
+    n = side * side
+    idx = np.arange(n).reshape(side, side)
+    pairs = np.concatenate([np.stack([idx[:, :-1].ravel(), idx[:, 1:].ravel()], 1),
+                            np.stack([idx[:-1, :].ravel(), idx[1:, :].ravel()], 1)])
+    wts = rng.integers(1, 4, len(pairs))
+    src = np.concatenate([pairs[:, 0], pairs[:, 1]])
+    dst = np.concatenate([pairs[:, 1], pairs[:, 0]])
+    ww = np.concatenate([wts, wts])
+    order = np.lexsort((dst, src))
+    ix, w = dst[order].astype(np.int64), ww[order].astype(np.int64)
+    ip = np.concatenate(([0], np.cumsum(np.bincount(src, minlength=n)))).astype(np.int64)
+    nw = np.ones(n, dtype=np.int64)
+    nb = 300
+    a = np.minimum((np.arange(n) + rng.integers(-200, 200, n)) // (n // nb), nb - 1).clip(0).astype(np.int64)
+    cap = n // nb + 20
+    for use_w in (1, 0):
+        a1, a2 = a.copy(), a.copy()
+        bw1 = np.bincount(a1, weights=nw, minlength=nb).astype(np.int64)
+        bw2 = bw1.copy()
+        total, moves = 0, np.zeros(1, dtype=np.int64)
+        for _ in range(8):
+            _native.call("mp_refine_boundary_pass", n, p(ip), p(ix), p(w), p(a2), p(bw2), nb, p(nw), cap, use_w,
+                         p(moves))
+            total += int(moves[0])
+            if moves[0] == 0:
+                break
+        assert total > 0
+        _native.call("mp_refine_boundary", n, p(ip), p(ix), p(w), p(a1), p(bw1), nb, p(nw), cap, use_w, 8, p(moves))
+        assert np.array_equal(a1, a2) and np.array_equal(bw1, bw2) and int(moves[0]) == total
