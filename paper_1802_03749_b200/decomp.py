@@ -144,12 +144,13 @@ class ThreadTransport:
         self.hub, self.rank = hub, rank
 
     def exchange(self, send: dict, recv: dict) -> None:
+        copies = {peer: t.clone() for peer, t in send.items()}
         if any(t.is_cuda for t in send.values()):
-            torch.cuda.current_stream().synchronize()
-        for peer, t in send.items():
-            self.hub.box(self.rank, peer).put(t.clone())
+            torch.cuda.current_stream().synchronize()  # packed and cloned before a peer reads them
+        for peer, t in copies.items():
+            self.hub.box(self.rank, peer).put(t)
         for peer, t in recv.items():
-            t.copy_(self.hub.box(peer, self.rank).get())
+            t.copy_(self.hub.box(peer, self.rank).get(timeout=120))  # a failed peer raises queue.Empty
 
 
 class HaloExchange:
@@ -211,7 +212,8 @@ def slab_bounds(nx: int, ny: int, world: int):
 class DistributedLoop:
     """One rank's share of a decomposed flux-type loop: local plan + halo."""
 
-    def __init__(self, mesh_local, kernel, dec: Decomposition, transport, config, schedule="dataflow"):
+    def __init__(self, mesh_local, kernel, dec: Decomposition, transport, config, schedule="dataflow",
+                 overlap=None):
         import paper_1802_03749_b200 as mp
 
         self.plan = mp.build_hierarchical_plan(mesh_local, kernel, config)
@@ -223,11 +225,46 @@ class DistributedLoop:
         self.inc = kernel.increment_args[0].array
         self.rc = None if self.read is None else mesh_local.data[self.read].components
         self.ic = mesh_local.data[self.inc].components
+        # core / boundary split: core blocks touch no halo point, so
+        # they run while the halo import is in flight; the colour schedules only
+        if overlap is None:
+            overlap = not schedule.endswith("dataflow") and self.read is not None
+        self.core = self.boundary = None
+        if overlap:
+            core = self.core_blocks()
+            self.core = self.plan._device.subset(core)
+            self.boundary = self.plan._device.subset(~core)
+            self.comm = torch.cuda.Stream()
+
+    def core_blocks(self) -> torch.Tensor:
+        """Per block of the local plan: true when none of its elements
+        references a halo point (plan numbering)."""
+        dp = self.plan._device
+        halo = torch.zeros(self.dec.n_local, dtype=torch.bool, device=dp.map.device)
+        if self.halo.all_halo is not None:
+            halo[self.halo.all_halo.long()] = True
+        touch = halo[dp.map.long()].any(1).to(torch.int32)
+        bo = dp.block_offsets.long()
+        nb = bo.numel() - 1
+        per_block = torch.zeros(nb, dtype=torch.int32, device=touch.device)
+        if nb:
+            blk = torch.repeat_interleave(torch.arange(nb, device=touch.device), bo[1:] - bo[:-1])
+            per_block.index_add_(0, blk, touch)
+        return per_block == 0
 
     def step(self) -> None:
-        if self.read is not None:
-            self.halo.import_rows(self.loop.tensors[self.read], self.rc)
-        self.loop.run()
+        if self.core is None:
+            if self.read is not None:
+                self.halo.import_rows(self.loop.tensors[self.read], self.rc)
+            self.loop.run()
+        else:
+            cur = torch.cuda.current_stream()
+            self.comm.wait_stream(cur)       # this step's inputs are in place
+            self.loop.run(sub=self.core)     # enqueued first: runs while the import is in flight
+            with torch.cuda.stream(self.comm):
+                self.halo.import_rows(self.loop.tensors[self.read], self.rc)
+            cur.wait_stream(self.comm)
+            self.loop.run(sub=self.boundary)
         self.halo.export_increments(self.loop.tensors[self.inc], self.ic)
 
     def step_host(self, inputs: dict, out) -> None:
@@ -245,6 +282,8 @@ class DistributedLoop:
         return v[pf[: self.dec.n_owned]]
 
     def launches_per_step(self) -> int:
+        if self.core is not None:
+            return self.core.launches + self.boundary.launches + self.halo.launches_per_step()
         return self.loop.launches_per_run() + self.halo.launches_per_step()
 
 

@@ -170,10 +170,20 @@ class DeviceLoop:
     launches: int = 0
     _keep: list = field(default_factory=list)
 
-    def run(self, stream=None) -> None:
-        """Launch one full execution of the loop (all colours); asynchronous."""
+    def run(self, stream=None, sub=None) -> None:
+        """Launch one full execution of the loop (all colours); asynchronous.
+        ``sub`` (a DevicePlan.subset view, colour schedules only) runs only
+        that view's blocks."""
         sp = _native.stream_ptr(stream)
         dp = self.plan._device
+        if sub is not None:
+            if isinstance(self.plan, GlobalPlan) or self.pipelined == "atomic" or \
+                    self.schedule & 3 == _native.MP_SCHED_DATAFLOW:
+                raise KernelSpecError("block subsets run under the colour schedules of a hierarchical plan")
+            fn = ("mp_exec_hier_stream" if self.pipelined == "stream" else
+                  "mp_exec_hier_pipelined" if self.pipelined else "mp_exec_hier")
+            _native.call(fn, self.loop, sub.struct, self.schedule, 1, sp)
+            return
         if self.pipelined == "atomic":
             _native.call("mp_exec_atomic", self.loop, sp)
         elif isinstance(self.plan, GlobalPlan):

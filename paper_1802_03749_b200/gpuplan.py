@@ -25,6 +25,7 @@ Device tensors that the executors need stay resident in a ``DevicePlan``.
 
 from dataclasses import dataclass
 
+import ctypes
 import os
 
 import numpy as np
@@ -273,6 +274,17 @@ def split_oversized(offsets: np.ndarray, limit: int) -> np.ndarray:
 
 
 @dataclass
+class SubPlan:
+    """A block subset of a DevicePlan (DevicePlan.subset): the C struct, the
+    number of kept blocks and colour launches, and the arrays it points to."""
+
+    struct: object
+    num_blocks: int
+    launches: int
+    keep: list
+
+
+@dataclass
 class DevicePlan:
     """Device-resident execution structures of one hierarchical plan."""
 
@@ -409,6 +421,36 @@ class DevicePlan:
         p.tpred_pad = self.tpred_pad.data_ptr()
         p.tblock_colour = self.tblock_colour.data_ptr()
         return p
+
+    def subset(self, block_mask: torch.Tensor) -> "SubPlan":
+        """A view of the plan restricted to the blocks where ``block_mask`` is
+        true, for the colour schedules: the same element, staging and pull
+        arrays, with each colour's ticket list cut to the kept blocks (in the
+        same order).  Running the views of a split of the blocks one after the
+        other runs every block once, each colour race-free; a point touched by
+        both views gets the first view's increments first."""
+        if self.elem_meta is None:
+            self.finish_stream()
+        dev = self.blocks_by_colour.device
+        nb = self.block_offsets.numel() - 1
+        offs = np.asarray(self.colour_block_offsets, dtype=np.int64)
+        keep = block_mask.to(dev)[self.blocks_by_colour.long()] if nb else torch.zeros(0, dtype=torch.bool, device=dev)
+        idx = torch.nonzero(keep).flatten()
+        ticket_colour = np.repeat(np.arange(len(offs) - 1), np.diff(offs))
+        kept_colour = ticket_colour[idx.cpu().numpy()]
+        sub_offs = np.zeros(len(offs), dtype=np.int32)
+        sub_offs[1:] = np.cumsum(np.bincount(kept_colour, minlength=len(offs) - 1))
+        bbc = self.blocks_by_colour[idx].contiguous()
+        tdesc = self.tdesc_colour.reshape(-1, 4)[idx].contiguous() if nb else self.tdesc_colour
+        base = self.struct()
+        p = _native.MpHierPlan()
+        ctypes.pointer(p)[0] = base
+        p.num_blocks = int(idx.numel())
+        p.blocks_by_colour = bbc.data_ptr()
+        p.colour_block_offsets_host = sub_offs.ctypes.data
+        p.tdesc_colour = tdesc.data_ptr()
+        p.tblock_colour = bbc.data_ptr()
+        return SubPlan(p, int(idx.numel()), int(np.count_nonzero(np.diff(sub_offs))), [bbc, tdesc, sub_offs])
 
     def reschedule(self, lag: int) -> None:
         """Recompute the dataflow order for another lag (tuning)."""

@@ -134,9 +134,14 @@ def test_decompose_lists_consistent():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,reorder,schedule", [(2, "gps", "dataflow"), (3, "none", "dataflow"),
-                                                    (4, "gps", "stream"), (2, "none", "stream-pull")])
-def test_threaded_ranks_on_one_gpu_match_serial(world, reorder, schedule):
+@pytest.mark.parametrize("world,reorder,schedule,overlap", [
+    (2, "gps", "dataflow", False), (3, "none", "dataflow", False), (4, "gps", "stream", False),
+    (2, "none", "stream-pull", False), (4, "gps", "stream", True), (2, "none", "stream-pull", True),
+    (3, "gps", "colour", True), (2, "gps", "pipelined", True)])
+def test_threaded_ranks_on_one_gpu_match_serial(world, reorder, schedule, overlap):
+    """Decomposed steps (halo import, local loop, increment export) equal the
+    serial loop; with ``overlap`` the core blocks (no halo point) run while the
+    import is in flight and the boundary blocks after it."""
     import threading
 
     import paper_1802_03749_b200 as mp
@@ -157,15 +162,33 @@ def test_threaded_ranks_on_one_gpu_match_serial(world, reorder, schedule):
     out, errors = {}, []
 
     def rank_main(r):
+        torch.cuda.set_device(0)
+        # each simulated rank on its own stream (separate processes each have
+        # their own default stream; threads would share the legacy one)
+        with torch.cuda.stream(torch.cuda.Stream()):
+            rank_body(r)
+
+    def rank_body(r):
         try:
-            torch.cuda.set_device(0)
             t, g = tables[r]
             dec = decomp.decompose(t, g, bounds, r, world, lambda obj: halos)
             res0 = np.zeros((dec.n_local, 4))
             local = decomp.local_flux_mesh(t, g, dec, q[dec.local_points], w[g], res0)
             kernel = mp.kernel_for_mesh("flux", local)
             dl = decomp.DistributedLoop(local, kernel, dec, decomp.ThreadTransport(hub, r),
-                                        mp.PlanConfig(reorder=reorder, block_size=64), schedule)
+                                        mp.PlanConfig(reorder=reorder, block_size=64), schedule, overlap=overlap)
+            if overlap:
+                core = dl.core_blocks().cpu().numpy()
+                dp = dl.plan._device
+                halo = np.zeros(dec.n_local, dtype=bool)
+                for rows in dl.dec.halo_rows.values():
+                    halo[rows] = True
+                bo = dp.block_offsets.cpu().numpy()
+                tab = dp.map.cpu().numpy()
+                for b in range(len(bo) - 1):
+                    assert core[b] == (not halo[tab[bo[b]:bo[b + 1]]].any())
+                assert dl.core.num_blocks + dl.boundary.num_blocks == dl.plan.num_blocks
+                assert (dl.boundary.num_blocks > 0) == bool(halo.any())  # the last slab imports nothing
             for _ in range(3):
                 dl.step()
             torch.cuda.synchronize()

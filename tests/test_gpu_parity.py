@@ -463,3 +463,31 @@ def test_atomic_baseline_exact_on_grid_data(family, dims, kname):
     arr = plan.mesh.data[inc]
     res = plan.mesh.with_data(mp.DataArray(arr.name, arr.set, arr.components, lp.tensors[inc].cpu().numpy(), arr.layout))
     assert np.array_equal(_v2(plan.restore_data(res), inc), want)
+
+
+@pytest.mark.parametrize("kname,family,dims", [("flux", "quad2d", (200, 150)), ("scatter8", "hex3d-nodes", (14, 12, 10)),
+                                               ("face-flux", "hex3d-faces", (12, 10, 9))])
+def test_block_subsets_cover_the_loop(kname, family, dims):
+    """DevicePlan.subset views (the decomposition's core / boundary split):
+    running a random split of the blocks as two views equals one full run on
+    grid data (each point's increments only change association), every colour
+    schedule and executor."""
+    mesh = mp.generate_mesh(family, dims, dtype="f64")
+    kernel = mp.kernel_for_mesh(kname, mesh)
+    staging = "increment-only" if kname == "face-flux" else "all-indirect"
+    plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps", staging=staging, block_size=64))
+    inc = INC_OF[kname]
+    g = torch.Generator(device="cuda").manual_seed(3)
+    mask = torch.rand(plan.num_blocks, generator=g, device="cuda") < 0.6
+    for sched in ("stream", "stream-pull", "colour", "pipelined"):
+        full = mp.bind(plan, kernel, schedule=sched)
+        full.run()
+        split = mp.bind(plan, kernel, schedule=sched)
+        a, b = plan._device.subset(mask), plan._device.subset(~mask)
+        assert a.num_blocks + b.num_blocks == plan.num_blocks
+        split.run(sub=a)
+        split.run(sub=b)
+        torch.cuda.synchronize()
+        assert bit_equal(split.tensors[inc].cpu().numpy(), full.tensors[inc].cpu().numpy()), sched
+    with pytest.raises(mp.KernelSpecError):
+        mp.bind(plan, kernel, schedule="stream-dataflow").run(sub=a)
