@@ -322,6 +322,11 @@ def our_arm(args):
     # atomics baseline (the paper's other race-avoidance strategy) on the same
     # element order and layout as the hierarchical plan
     results["atomic"] = time_steps(mp.bind(hier, kernel, schedule="atomic").run, args.steps, args.warmup, flush)
+    # and the temporary-array strategy (per-(element, slot) temps + per-point
+    # fold in element order: the serial loop's result, bit for bit)
+    tmp_loop = mp.bind(hier, kernel, schedule="temp-array")
+    results["temp_array"] = time_steps(tmp_loop.run, args.steps, args.warmup, flush)
+    del tmp_loop
 
     if args.schedule == "best":
         args.schedule = min(SCHEDULES, key=lambda sc: statistics.median(results[f"hier_{sc}"]))
@@ -386,6 +391,8 @@ def our_arm(args):
             "speedup_hier_over_global": round(ms_glob / ms, 3),
             "atomic_ms": round(statistics.median(results["atomic"]), 5),
             "speedup_hier_over_atomic": round(statistics.median(results["atomic"]) / ms, 3),
+            "temp_array_ms": round(statistics.median(results["temp_array"]), 5),
+            "speedup_hier_over_temp_array": round(statistics.median(results["temp_array"]) / ms, 3),
             "block_colours": hier.block_colours.num_colours, "num_blocks": hier.num_blocks,
             "reuse_factor": round(mp.reuse_factor(hier), 4),
             "thread_colours_mean": round(float(hier.thread_colour_counts.mean()), 3),

@@ -37,6 +37,10 @@ SCHEDULES = {
     "stream-pull": (_native.MP_SCHED_COLOUR | _native.MP_SCHED_PULL, "stream"),
     # comparison baseline (not bit-exact: atomics reassociate): ignores the colouring
     "atomic": (_native.MP_SCHED_COLOUR, "atomic"),
+    # comparison baseline (the paper's temporary-array strategy; bit-identical
+    # to execute_serial on the plan's numbering): per-(element, slot) temp
+    # increments, then a per-point fold in element order
+    "temp-array": (_native.MP_SCHED_COLOUR, "temp-array"),
 }
 TORCH_DTYPES = {"f64": torch.float64, "f32": torch.float32, "i64": torch.int64, "i32": torch.int32}
 
@@ -177,7 +181,7 @@ class DeviceLoop:
         sp = _native.stream_ptr(stream)
         dp = self.plan._device
         if sub is not None:
-            if isinstance(self.plan, GlobalPlan) or self.pipelined == "atomic" or \
+            if isinstance(self.plan, GlobalPlan) or self.pipelined in ("atomic", "temp-array") or \
                     self.schedule & 3 == _native.MP_SCHED_DATAFLOW:
                 raise KernelSpecError("block subsets run under the colour schedules of a hierarchical plan")
             fn = ("mp_exec_hier_stream" if self.pipelined == "stream" else
@@ -186,6 +190,9 @@ class DeviceLoop:
             return
         if self.pipelined == "atomic":
             _native.call("mp_exec_atomic", self.loop, sp)
+        elif self.pipelined == "temp-array":
+            off, refs, temp = self._keep[-3:]
+            _native.call("mp_exec_serial", self.loop, off.data_ptr(), refs.data_ptr(), temp.data_ptr(), sp)
         elif isinstance(self.plan, GlobalPlan):
             offs = np.ascontiguousarray(dp.colour_offsets, dtype=np.int64)
             _native.call("mp_exec_global", self.loop, offs.ctypes.data, len(offs) - 1,
@@ -225,8 +232,9 @@ class DeviceLoop:
         dst.copy_(self.tensors[inc].reshape(dst.shape), non_blocking=True)
 
     def launches_per_run(self) -> int:
-        if self.pipelined == "atomic":
-            return 1 if self.plan.mesh.sets[self.kernel.iter_set_name(self.plan.mesh)].size else 0
+        if self.pipelined in ("atomic", "temp-array"):
+            n = 1 if self.plan.mesh.sets[self.kernel.iter_set_name(self.plan.mesh)].size else 0
+            return n * (2 if self.pipelined == "temp-array" else 1)
         if isinstance(self.plan, GlobalPlan):
             return int(np.count_nonzero(np.diff(self.plan._device.colour_offsets)))
         if self.schedule & 3 == _native.MP_SCHED_DATAFLOW:
@@ -276,7 +284,13 @@ def bind(plan, kernel: KernelSpec, tensors: dict | None = None, schedule: str = 
     if schedule not in SCHEDULES:
         raise KernelSpecError(f"unknown schedule {schedule!r}; expected one of {sorted(SCHEDULES)}")
     sched, pipelined = SCHEDULES[schedule]
-    return DeviceLoop(plan, kernel, t, L, sched, pipelined)
+    keep = []
+    if pipelined == "temp-array":
+        off, refs = _serial_refs(plan._device.map, sorted(kernel.arg_slots(mesh, inc)), m.to_set.size)
+        temp = torch.empty(max(m.from_set.size * m.arity * inc_arr.components, 1),
+                           dtype=TORCH_DTYPES[inc_arr.elem_type], device=dev)
+        keep = [off, refs, temp]
+    return DeviceLoop(plan, kernel, t, L, sched, pipelined, _keep=keep)
 
 
 # ------------------------------------------------------------------------------
@@ -464,6 +478,24 @@ def execute_hierarchical(plan: HierarchicalPlan, kernel: KernelSpec, schedule: s
     return _run_and_collect(plan, kernel, schedule)
 
 
+def _serial_refs(map_d: torch.Tensor, wslots, npts: int):
+    """Per point, its (element*arity + slot) references through the written
+    slots in element order (np.add.at's order): int32 CSR (offsets, refs)."""
+    dev = map_d.device
+    n, ar = map_d.shape
+    flat = map_d.long().reshape(-1)
+    pos = torch.arange(n * ar, dtype=torch.long, device=dev)
+    in_w = (pos % max(ar, 1)).unsqueeze(0) == torch.as_tensor(wslots, device=dev).unsqueeze(1) if wslots else None
+    sel = in_w.any(0) if in_w is not None else torch.zeros_like(pos, dtype=torch.bool)
+    keys, order = torch.sort(flat[sel], stable=True)
+    refs = pos[sel][order]
+    # temp is indexed by e*arity + s of the op's own slot loop
+    off = torch.zeros(npts + 1, dtype=torch.int32, device=dev)
+    if keys.numel():
+        off[1:] = torch.cumsum(torch.bincount(keys, minlength=npts), 0).to(torch.int32)
+    return off, refs.to(torch.int32)
+
+
 def execute_serial(mesh: Mesh, kernel: KernelSpec) -> Mesh:
     """Element-order semantics of the reference oracle, computed on the GPU:
     temp-array increments + per-point ordered folds (bit-identical to
@@ -475,17 +507,7 @@ def execute_serial(mesh: Mesh, kernel: KernelSpec) -> Mesh:
     dev = torch.device("cuda")
     n, ar = m.from_set.size, m.arity
     map_d = torch.as_tensor(m.table, device=dev).to(torch.int32).reshape(n, ar)
-    wslots = sorted(kernel.arg_slots(mesh, inc))
-    flat = map_d.long().reshape(-1)
-    pos = torch.arange(n * ar, dtype=torch.long, device=dev)
-    in_w = (pos % max(ar, 1)).unsqueeze(0) == torch.as_tensor(wslots, device=dev).unsqueeze(1) if wslots else None
-    sel = in_w.any(0) if in_w is not None else torch.zeros_like(pos, dtype=torch.bool)
-    keys, order = torch.sort(flat[sel], stable=True)
-    refs = pos[sel][order]
-    # temp is indexed by e*arity + s of the op's own slot loop
-    off = torch.zeros(m.to_set.size + 1, dtype=torch.int32, device=dev)
-    if keys.numel():
-        off[1:] = torch.cumsum(torch.bincount(keys, minlength=m.to_set.size), 0).to(torch.int32)
+    off, refs = _serial_refs(map_d, sorted(kernel.arg_slots(mesh, inc)), m.to_set.size)
     arrays = {}
     for a in (ind, dr, inc):
         if a is not None:
@@ -505,7 +527,6 @@ def execute_serial(mesh: Mesh, kernel: KernelSpec) -> Mesh:
     L.dir_read, L.dir_comps = arrays[dr.array][0].data_ptr(), mesh.data[dr.array].components
     L.inc, L.inc_comps = arrays[inc.array][0].data_ptr(), inc_arr.components
     temp = torch.empty(max(n * ar * inc_arr.components, 1), dtype=TORCH_DTYPES[inc_arr.elem_type], device=dev)
-    refs32 = refs.to(torch.int32)
-    _native.call("mp_exec_serial", L, off.data_ptr(), refs32.data_ptr(), temp.data_ptr(), _native.stream_ptr())
+    _native.call("mp_exec_serial", L, off.data_ptr(), refs.data_ptr(), temp.data_ptr(), _native.stream_ptr())
     out = arrays[inc.array][0].cpu().numpy()
     return mesh.with_data(DataArray(inc_arr.name, inc_arr.set, inc_arr.components, out, arrays[inc.array][1]))

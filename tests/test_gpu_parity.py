@@ -491,3 +491,35 @@ def test_block_subsets_cover_the_loop(kname, family, dims):
         assert bit_equal(split.tensors[inc].cpu().numpy(), full.tensors[inc].cpu().numpy()), sched
     with pytest.raises(mp.KernelSpecError):
         mp.bind(plan, kernel, schedule="stream-dataflow").run(sub=a)
+
+
+@pytest.mark.parametrize("family,dims,kname", [("quad2d", (64, 48), "flux"), ("hex3d-nodes", (10, 9, 8), "scatter8"),
+                                               ("hex3d-faces", (9, 8, 7), "face-flux"), ("tri2d", (30, 20), "flux")])
+def test_temp_array_baseline_is_serial_order(family, dims, kname):
+    """Temporary-array baseline (per-(element, slot) temp increments, then a
+    per-point fold in element order): bit-identical to the serial loop over
+    the plan's numbering for arbitrary (non-grid) data."""
+    from oracle import loops
+
+    mesh = mp.generate_mesh(family, dims, dtype="f64")
+    rng = np.random.default_rng(5)
+    for name, arr in list(mesh.data.items()):
+        mesh = mesh.with_data(mp.DataArray(arr.name, arr.set, arr.components,
+                                           rng.standard_normal(arr.values.size), arr.layout))
+    kernel = mp.kernel_for_mesh(kname, mesh)
+    inc = INC_OF[kname]
+    staging = "increment-only" if kname == "face-flux" else "all-indirect"
+    plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps", staging=staging))
+    pm = plan.mesh
+    m = next(iter(pm.mappings.values()))
+    read = {"flux": "q", "face-flux": "state"}.get(kname)
+    direct = {"flux": "w", "scatter8": "stress", "face-flux": "facew"}[kname]
+    want = loops.serial_loop(kname, m.table, None if read is None else pm.data[read].view2d(),
+                             np.ascontiguousarray(pm.data[direct].view2d()), _v2(pm, inc))
+    lp = mp.bind(plan, kernel, schedule="temp-array")
+    assert lp.launches_per_run() == 2
+    lp.run()
+    torch.cuda.synchronize()
+    arr = pm.data[inc]
+    got = pm.with_data(mp.DataArray(arr.name, arr.set, arr.components, lp.tensors[inc].cpu().numpy(), arr.layout))
+    assert bit_equal(_v2(got, inc), want)
