@@ -347,14 +347,29 @@ def bench_rank(args, rank: int, world: int) -> int:
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
+    # a rank's share of the loop's bytes; below twice L2 the steps are timed
+    # one by one with L2 flushed in between (as bench.py does on one GPU)
+    share = (nx * ny * 4 * 8 * 3 + (nx * (ny - 1) + ny * (nx - 1)) * (2 * 8 + 2 * 4)) / world
+    flush = bench.L2Flusher(share < 2 * bench.L2_BYTES)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(args.steps):
-        dl.step()
-    b.record()
-    torch.cuda.synchronize()
+    if flush.buf is None:
+        a.record()
+        for _ in range(args.steps):
+            dl.step()
+        b.record()
+        torch.cuda.synchronize()
+        step_ms = a.elapsed_time(b) / args.steps
+    else:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for ea, eb in evs:
+            flush()
+            ea.record()
+            dl.step()
+            eb.record()
+        torch.cuda.synchronize()
+        step_ms = sum(ea.elapsed_time(eb) for ea, eb in evs) / args.steps
     dist.barrier()
-    ms = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+    ms = torch.tensor([step_ms], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     clocks = sampler.stop()
     # end to end: pinned host copies of this rank's arrays -> H2D -> step -> D2H
@@ -390,7 +405,8 @@ def bench_rank(args, rank: int, world: int) -> int:
             "config": {"workload": f"{args.config}: quad2d {nx}x{ny} flux f64 decomposed into {world} x-slabs",
                        "strategy": "hier", "reorder": args.reorder, "schedule": sched,
                        "parallelism": f"owner-compute x{world}, NCCL halo exchange",
-                       "useful_bytes_per_step": ub_total, "l2": "inputs larger than L2 (no flush)"},
+                       "useful_bytes_per_step": ub_total,
+                       "l2": "inputs larger than L2 (no flush)" if flush.buf is None else "flushed between steps"},
             "roofline": {"bound": "hbm", "achieved": round(gbps / world, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(gbps / world / peak, 4), "traffic": None, "peak_kind": kind,
                          "note": "per-GPU share of the whole-job effective bandwidth"},
