@@ -242,6 +242,46 @@ class DeviceLoop:
         return int(np.count_nonzero(np.diff(self.plan._device.colour_block_offsets)))
 
 
+class HostStream:
+    """Loop executions streamed over host buffers: every step copies its
+    inputs host -> device, runs the loop and copies the incremented array
+    back, like ``DeviceLoop.run_host``, but consecutive steps go to
+    ``depth`` CUDA streams with their own device arrays, so one step's
+    device -> host copy and the next step's host -> device copy and compute
+    overlap (the copy engines work both directions at once).  Pass a
+    different ``out`` buffer to steps that may be in flight together."""
+
+    def __init__(self, plan, kernel: KernelSpec, schedule: str = "stream", depth: int = 2):
+        self.loops = [bind(plan, kernel, schedule=schedule) for _ in range(depth)]
+        self.streams = [torch.cuda.Stream() for _ in range(depth)]
+        self.k = 0
+
+    def step(self, inputs: dict, out) -> None:
+        """Enqueue one step (asynchronous; ``synchronize`` waits for all)."""
+        i = self.k % len(self.loops)
+        self.k += 1
+        s = self.streams[i]
+        with torch.cuda.stream(s):
+            self.loops[i].run_host(inputs, out, stream=s)
+
+    def wait_on(self, event) -> None:
+        for s in self.streams:
+            s.wait_event(event)
+
+    def join(self, stream=None) -> None:
+        """Make ``stream`` (default: the current one) wait for every step enqueued so far."""
+        cur = stream or torch.cuda.current_stream()
+        for s in self.streams:
+            cur.wait_stream(s)
+
+    def synchronize(self) -> None:
+        for s in self.streams:
+            s.synchronize()
+
+    def launches_per_step(self) -> int:
+        return self.loops[0].launches_per_run()
+
+
 def _array_tensor(arr: DataArray, dev) -> torch.Tensor:
     host = torch.from_numpy(np.ascontiguousarray(arr.values))
     return host.to(dev, non_blocking=True)
