@@ -262,7 +262,9 @@ mp_status mp_initial_partition(int64_t n, const int64_t* indptr, const int64_t* 
  * _accel.heavy_edge_matching at partition.py:317): the same matching as the
  * sequential visit-order greedy, computed in dependency rounds (a node acts
  * once every earlier-visited node within two hops is matched).  `rounds`
- * receives the number of rounds. */
+ * receives the number of rounds; after 4096 rounds (MESHPLAN_MATCH_ROUNDS)
+ * the remaining turns finish on the host, still exact, and `rounds` is
+ * negated. */
 mp_status mp_heavy_edge_matching_device(int32_t n, const int64_t* indptr, const int64_t* indices,
                                         const int64_t* weights, const int64_t* node_w, const int64_t* visit,
                                         int64_t max_cluster, int64_t* match, int32_t* rounds, void* stream);

@@ -7,6 +7,9 @@
 //     to the reference's sequential visit-order greedy
 #include <cub/cub.cuh>
 #include <limits.h>
+#include <stdlib.h>
+
+#include <vector>
 
 #include "mp_common.cuh"
 
@@ -446,6 +449,12 @@ extern "C" mp_status mp_bfs_levels(int32_t n, const int64_t* indptr, const int32
   return MP_OK;
 }
 
+static int32_t hem_round_cap() {
+  const char* e = getenv("MESHPLAN_MATCH_ROUNDS");  // test hook: force the host finish
+  const int v = e ? atoi(e) : 0;
+  return v > 0 ? v : 4096;
+}
+
 extern "C" mp_status mp_heavy_edge_matching_device(int32_t n, const int64_t* indptr, const int64_t* indices,
                                                    const int64_t* weights, const int64_t* node_w,
                                                    const int64_t* visit, int64_t max_cluster, int64_t* match,
@@ -467,7 +476,8 @@ extern "C" mp_status mp_heavy_edge_matching_device(int32_t n, const int64_t* ind
   cudaError_t ce = cudaGetLastError();
   int32_t m = n, r = 0;
   int32_t *cur = wa.as<int32_t>(), *nxt = wb.as<int32_t>();
-  while (ce == cudaSuccess && m > 0) {
+  const int32_t cap = hem_round_cap();
+  while (ce == cudaSuccess && m > 0 && r < cap) {
     if ((ce = cudaMemsetAsync(cnt.p, 0, 4, st))) break;
     hem_round_kernel<<<grid_for(m), 256, 0, st>>>(m, cur, indptr, indices, weights, node_w, rk.as<int32_t>(),
                                                   max_cluster, match, dec.as<int64_t>());
@@ -482,5 +492,40 @@ extern "C" mp_status mp_heavy_edge_matching_device(int32_t n, const int64_t* ind
   cudaFreeHost(pinned);
   MP_CUDA_TRY(ce);
   *rounds = r;
+  if (m > 0) {
+    // A dependency chain longer than the round cap (adversarial visit orders;
+    // random ones need O(log n) rounds): finish sequentially on the host.  The
+    // decided nodes are the sequential outcomes and no decided node lies within
+    // two hops of an undecided one with a lower rank, so the remaining turns in
+    // visit order see exactly the sequential state.
+    std::vector<int64_t> ip(n + 1), w_match(n), vis(n), nw(n);
+    MP_CUDA_TRY(cudaMemcpyAsync(ip.data(), indptr, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+    MP_CUDA_TRY(cudaMemcpyAsync(w_match.data(), match, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    MP_CUDA_TRY(cudaMemcpyAsync(vis.data(), visit, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    MP_CUDA_TRY(cudaMemcpyAsync(nw.data(), node_w, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    MP_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<int64_t> ix(ip[n]), ew(ip[n]);
+    MP_CUDA_TRY(cudaMemcpy(ix.data(), indices, ip[n] * 8, cudaMemcpyDeviceToHost));
+    MP_CUDA_TRY(cudaMemcpy(ew.data(), weights, ip[n] * 8, cudaMemcpyDeviceToHost));
+    for (int32_t step = 0; step < n; ++step) {
+      const int64_t u = vis[step];
+      if (w_match[u] >= 0) continue;
+      int64_t best = u, best_w = -1;
+      for (int64_t j = ip[u]; j < ip[u + 1]; ++j) {
+        const int64_t v = ix[j];
+        if (w_match[v] >= 0 || v == u) continue;
+        if (nw[u] + nw[v] > max_cluster) continue;
+        if (ew[j] > best_w || (ew[j] == best_w && v < best)) {
+          best = v;
+          best_w = ew[j];
+        }
+      }
+      w_match[u] = best;
+      if (best != u) w_match[best] = u;
+    }
+    MP_CUDA_TRY(cudaMemcpyAsync(match, w_match.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    MP_CUDA_TRY(cudaStreamSynchronize(st));
+    *rounds = -r;  // negative: finished on the host after r rounds
+  }
   return MP_OK;
 }

@@ -57,3 +57,28 @@ def test_partition_device_matching_equals_host(monkeypatch):
     monkeypatch.setenv("MESHPLAN_HOST_MATCHING", "1")
     b = kway.partition_kway(g, cfg)
     assert np.array_equal(a.assignment, b.assignment) and a.cut == b.cut
+
+
+@pytest.mark.parametrize("cap", ["1", "2", "5"])
+def test_device_matching_host_finish_after_round_cap(cap, monkeypatch):
+    """Past the round cap the remaining turns run on the host in visit order:
+    still the sequential matching."""
+    monkeypatch.setenv("MESHPLAN_MATCH_ROUNDS", cap)
+    for seed in range(6):
+        ip, ix, w, rng = _graph(seed + 50, n=int(np.random.default_rng(seed).integers(40, 300)))
+        n = len(ip) - 1
+        nw = rng.integers(1, 3, n).astype(np.int64)
+        visit = rng.permutation(n).astype(np.int64)
+        assert np.array_equal(_device_match(ip, ix, w, nw, visit, 4), _host_match(ip, ix, w, nw, visit, 4))
+
+
+def test_device_matching_path_graph_in_order():
+    """An adversarial order (a path visited end to end: one ready node per
+    round) still matches the sequential greedy."""
+    n = 3000
+    ip = np.concatenate(([0], np.cumsum([1] + [2] * (n - 2) + [1]))).astype(np.int64)
+    ix = np.concatenate([[1]] + [[u - 1, u + 1] for u in range(1, n - 1)] + [[n - 2]]).astype(np.int64)
+    w = np.ones(len(ix), dtype=np.int64)
+    nw = np.ones(n, dtype=np.int64)
+    visit = np.arange(n, dtype=np.int64)
+    assert np.array_equal(_device_match(ip, ix, w, nw, visit, 2), _host_match(ip, ix, w, nw, visit, 2))
