@@ -320,7 +320,8 @@ def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
     )
     dp = gpuplan.build_device_hier(
         map_d.contiguous(), offsets, block_colours.colours, block_colours.num_colours, tcol_sorted, tcounts,
-        st_off, st_ids, wr_off, wr_ids, smask, config.staging == "all-indirect", m.to_set.size, max_block,
+        st_off, st_ids, wr_off, wr_ids, smask, gpuplan.stage_reads(kernel, mesh, config.staging, smask),
+        m.to_set.size, max_block,
     )
     tm.mark("device_plan")
     object.__setattr__(plan, "_device", dp)

@@ -393,7 +393,7 @@ def _device_from_host(plan, kernel):
         return gpuplan.build_device_hier(
             map_d, offsets, np.asarray(plan.block_colours.colours, dtype=np.int64), plan.block_colours.num_colours,
             i32(plan.thread_colours), i32(plan.thread_colour_counts), i32(st[0]), i32(st[1]), i32(wr[0]), i32(wr[1]),
-            smask, plan.config.staging == "all-indirect", m.to_set.size,
+            smask, gpuplan.stage_reads(kernel, mesh, plan.config.staging, smask), m.to_set.size,
             int(np.diff(offsets).max()) if offsets.size > 1 else 0,
         )
     except CapacityError as exc:

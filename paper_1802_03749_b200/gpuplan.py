@@ -67,6 +67,21 @@ def slot_mask(kernel, mesh, args) -> int:
     return mask
 
 
+def stage_reads(kernel, mesh, staging: str, smask: int) -> bool:
+    """Whether the executors stage the indirect read rows in shared memory:
+    always under all-indirect staging, and under increment-only staging when
+    every read slot is also a staged (incremented) slot of the same mapping:
+    the read rows are then in the block's staged list anyway, and taking them
+    from shared memory instead of global (simulator.py:605-610) changes no
+    value -- the plan is untouched, only the executor's data movement."""
+    if staging == "all-indirect":
+        return True
+    reads = list(kernel.indirect_read_args)
+    if not reads or smask == 0:
+        return False
+    return slot_mask(kernel, mesh, reads) & ~smask == 0
+
+
 # ---------------------------------------------------------------------------------
 # reorderings
 # ---------------------------------------------------------------------------------

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--runs", type=int, default=3)
     ap.add_argument("--timed", type=int, default=1)
     ap.add_argument("--lags", default="")
+    ap.add_argument("--staging", default=None, help="override the config's staging")
     args = ap.parse_args()
 
     import torch
@@ -31,6 +32,7 @@ def main():
     import paper_1802_03749_b200 as mp
 
     mesh, kernel, staging = bench.make_mesh(args.config)
+    staging = args.staging or staging
     cfg = mp.PlanConfig(strategy=args.strategy, reorder=args.reorder, layout=args.layout, staging=staging,
                         block_size=args.block_size)
     t0 = time.perf_counter()
