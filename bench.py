@@ -37,7 +37,11 @@ sys.path.insert(0, str(REPO))
 #: SURVEY 8d), the reference's k-way partition for the face loop (the config
 #: names k-way partitioned blocks; ~50 s to plan at 24M faces)
 DEFAULT_REORDER = {"C1": "gps", "C2": "gps", "C3": "none", "C4": "partition", "C5": "gps"}
-COMPARE_REORDER = {"C2": ("none", "gps")}
+#: other block layouts timed beside the headline (reported as vs_layout):
+#: name -> (reorder, block size or None for --block-size, schedule or None for the headline's)
+COMPARE_REORDER = {"C2": (("none", None, None),),
+                   # the paper's handcrafted hex blocks (shape from tools/shape_sweep.sh)
+                   "C4": (("structured:4,4,8", 480, "stream-pull"),)}
 CONFIGS = {
     # name: (family, dims, kernel, dtype, staging)
     "C1": ("quad2d", (848, 848), "flux", "f64", "all-indirect"),
@@ -333,18 +337,22 @@ def our_arm(args):
     # the configs that compare block layouts (BASELINE.json configs[1]: natural
     # vs GPS-reordered) time the other layout with the headline schedule too
     vs_layout = {}
-    for other in COMPARE_REORDER.get(args.config, ()):
+    for other, bs, sched in COMPARE_REORDER.get(args.config, ()):
         if other == args.reorder:
             continue
         t0 = time.perf_counter()
         alt = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(
-            reorder=other, layout=args.layout, staging=staging, block_size=args.block_size))
+            reorder=other, layout=args.layout, staging=staging, block_size=bs or args.block_size))
         t_alt = time.perf_counter() - t0
-        ms_alt = statistics.median(time_steps(mp.bind(alt, kernel, schedule=args.schedule).run, args.steps,
-                                              args.warmup, flush))
+        sched = sched or args.schedule
+        alt_loop = mp.bind(alt, kernel, schedule=sched)
+        ms_alt = statistics.median(time_steps(alt_loop.run, args.steps, args.warmup, flush))
         vs_layout[other] = {"ms_per_step": round(ms_alt, 5), "gbps": round(ub / (ms_alt * 1e-3) / 1e9, 2),
+                            "frac": round(ub / (ms_alt * 1e-3) / 1e9 / hbm_peak()[0], 4),
+                            "block_size": bs or args.block_size, "schedule": sched,
                             "reuse_factor": round(mp.reuse_factor(alt), 4),
                             "block_colours": alt.block_colours.num_colours, "plan_build_s": round(t_alt, 2)}
+        del alt_loop, alt
     # end to end through the public API with host buffers (pinned), H2D + D2H in the region
     main = loops[args.schedule]
     inputs = {a.array: hier.mesh.data[a.array].values for a in kernel.args}
