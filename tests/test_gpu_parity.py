@@ -489,6 +489,13 @@ def test_block_subsets_cover_the_loop(kname, family, dims):
         split.run(sub=b)
         torch.cuda.synchronize()
         assert bit_equal(split.tensors[inc].cpu().numpy(), full.tensors[inc].cpu().numpy()), sched
+    empty = plan._device.subset(torch.zeros(plan.num_blocks, dtype=torch.bool, device="cuda"))
+    assert empty.num_blocks == 0 and empty.launches == 0
+    lp = mp.bind(plan, kernel, schedule="stream")
+    before = lp.tensors[inc].clone()
+    lp.run(sub=empty)
+    torch.cuda.synchronize()
+    assert torch.equal(lp.tensors[inc], before)
     with pytest.raises(mp.KernelSpecError):
         mp.bind(plan, kernel, schedule="stream-dataflow").run(sub=a)
 
@@ -545,3 +552,30 @@ def test_host_stream_steps_equal_single_runs():
             assert all(bit_equal(o.numpy(), want) for o in outs)
     hs.synchronize()
     assert bit_equal(outs[0].numpy(), want)
+
+
+@pytest.mark.parametrize("kname", ["face-flux", "face-flux-heavy"])
+def test_staged_reads_under_increment_only_change_nothing(kname, monkeypatch):
+    """Increment-only plans whose read slots are staged slots: the executors
+    take the read rows from the staged copy (gpuplan.stage_reads); results
+    are bit-identical to reading them from global, every schedule, random
+    data."""
+    from paper_1802_03749_b200 import gpuplan
+
+    mesh = mp.generate_mesh("hex3d-faces", (10, 9, 8), dtype="f64")
+    rng = np.random.default_rng(9)
+    for name, arr in list(mesh.data.items()):
+        mesh = mesh.with_data(mp.DataArray(arr.name, arr.set, arr.components,
+                                           rng.uniform(0.5, 1.5, arr.values.size), arr.layout))
+    kernel = mp.kernel_for_mesh(kname, mesh)
+    cfg = mp.PlanConfig(reorder="partition", staging="increment-only")
+    staged = mp.build_hierarchical_plan(mesh, kernel, cfg)
+    assert staged._device.stage_reads
+    monkeypatch.setattr(gpuplan, "stage_reads", lambda *a: False)
+    direct = mp.build_hierarchical_plan(mesh, kernel, cfg)
+    assert not direct._device.stage_reads
+    inc = INC_OF[kname]
+    for sched in SCHEDULES:
+        a, _ = mp.execute_hierarchical(staged, kernel, schedule=sched)
+        b, _ = mp.execute_hierarchical(direct, kernel, schedule=sched)
+        assert bit_equal(_v2(a, inc), _v2(b, inc)), sched
