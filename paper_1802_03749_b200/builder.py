@@ -184,7 +184,7 @@ def build_global(mesh: Mesh, kernel, config, hw) -> GlobalPlan:
     iter_set = kernel.iter_set_name(mesh)
     n = mesh.sets[iter_set].size
     fwd: dict = {}
-    map_d = torch.as_tensor(m.table, device=dev).to(torch.int32).reshape(n, m.arity)
+    map_d = gpuplan.upload(m.table, dev).to(torch.int32).reshape(n, m.arity)
     map_d, _, _ = _reorder(mesh, kernel, config, m, map_d, fwd)
 
     # per-element distinct written points (plan.py:201-229) -> greedy least-loaded
@@ -246,7 +246,7 @@ def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
     n = mesh.sets[iter_set].size
     S = config.block_size
     fwd: dict = {}
-    map_d = torch.as_tensor(m.table, device=dev).to(torch.int32).reshape(n, m.arity)
+    map_d = gpuplan.upload(m.table, dev).to(torch.int32).reshape(n, m.arity)
     tm.mark("upload")
     map_d, sizes, meta = _reorder(mesh, kernel, config, m, map_d, fwd)
     tm.mark("reorder")

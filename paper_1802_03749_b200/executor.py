@@ -367,7 +367,7 @@ def _kernel_map(plan, kernel) -> torch.Tensor:
     m = gpuplan.single_mapping(plan.mesh, kernel)
     if m is None:
         raise KernelSpecError(f"kernel {kernel.name!r} has no indirect argument")
-    return torch.as_tensor(m.table, device="cuda").to(torch.int32).contiguous()
+    return gpuplan.upload(m.table, "cuda").to(torch.int32).contiguous()
 
 
 def _device_from_host(plan, kernel):
@@ -546,7 +546,7 @@ def execute_serial(mesh: Mesh, kernel: KernelSpec) -> Mesh:
     _native.require_cuda()
     dev = torch.device("cuda")
     n, ar = m.from_set.size, m.arity
-    map_d = torch.as_tensor(m.table, device=dev).to(torch.int32).reshape(n, ar)
+    map_d = gpuplan.upload(m.table, dev).to(torch.int32).reshape(n, ar)
     off, refs = _serial_refs(map_d, sorted(kernel.arg_slots(mesh, inc)), m.to_set.size)
     arrays = {}
     for a in (ind, dr, inc):

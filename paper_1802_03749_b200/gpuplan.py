@@ -43,6 +43,16 @@ def _dev() -> torch.device:
     return torch.device(DEV)
 
 
+def upload(a: np.ndarray, dev) -> torch.Tensor:
+    """Host array -> device tensor; read-only arrays (mesh tables are frozen)
+    are copied from without torch's non-writable-array warning."""
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.as_tensor(a, device=dev)
+
+
 def _sp():
     return _native.stream_ptr()
 
