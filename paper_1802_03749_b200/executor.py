@@ -204,6 +204,24 @@ class DeviceLoop:
                   "mp_exec_hier_pipelined" if self.pipelined else "mp_exec_hier")
             _native.call(fn, self.loop, dp.struct_cached(), self.schedule, max(dp.epoch, 1), sp)
 
+    def capture(self):
+        """One execution captured as a CUDA graph (colour schedules: the
+        launches, with their programmatic-dependent edges, replay with one
+        submission).  Returns the ``torch.cuda.CUDAGraph``; ``replay()`` runs
+        the loop on the current stream's device.  Dataflow schedules stamp a
+        fresh epoch per execution and are not capturable."""
+        if self.schedule & 3 == _native.MP_SCHED_DATAFLOW and not isinstance(self.plan, GlobalPlan):
+            raise KernelSpecError("dataflow schedules take a new epoch per execution; capture a colour schedule")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.run(side)  # warm: kernel attributes and occupancy queries happen outside the capture
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run(torch.cuda.current_stream())
+        return g
+
     def run_host_inputs(self, inputs: dict) -> None:
         """Asynchronous H2D of the given arrays (name -> pinned numpy / torch,
         plan numbering) into the bound device tensors."""

@@ -579,3 +579,23 @@ def test_staged_reads_under_increment_only_change_nothing(kname, monkeypatch):
         a, _ = mp.execute_hierarchical(staged, kernel, schedule=sched)
         b, _ = mp.execute_hierarchical(direct, kernel, schedule=sched)
         assert bit_equal(_v2(a, inc), _v2(b, inc)), sched
+
+
+def test_captured_graph_replays_the_loop():
+    """DeviceLoop.capture: a CUDA-graph replay equals a direct execution,
+    bit for bit, for the colour schedules (dataflow refuses)."""
+    mesh = mp.generate_mesh("quad2d", (200, 160), dtype="f64")
+    kernel = mp.kernel_for_mesh("flux", mesh)
+    plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps"))
+    for sched in ("stream", "stream-pull", "pipelined", "colour"):
+        a = mp.bind(plan, kernel, schedule=sched)
+        b = mp.bind(plan, kernel, schedule=sched)
+        g = b.capture()  # runs b once (warm-up)
+        for _ in range(3):
+            a.run()
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        assert bit_equal(a.tensors["res"].cpu().numpy(), b.tensors["res"].cpu().numpy()), sched
+    with pytest.raises(mp.KernelSpecError):
+        mp.bind(plan, kernel, schedule="stream-dataflow").capture()
