@@ -3,6 +3,9 @@
 
 #include "mp_common.cuh"
 
+#include <mutex>
+#include <vector>
+
 namespace mp {
 namespace {
 thread_local std::string g_last_error;
@@ -20,6 +23,30 @@ void set_error(const char* fmt, ...) {
 void clear_error() { g_last_error.clear(); }
 
 const char* last_error() { return g_last_error.c_str(); }
+
+cudaError_t raise_smem_limit(const void* kern, size_t smem) {
+  struct Limit {
+    const void* k;
+    int dev;
+    size_t smem;
+  };
+  static std::mutex mu;
+  static std::vector<Limit> limits;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& l : limits)
+    if (l.k == kern && l.dev == dev) {
+      if (l.smem >= smem) return cudaSuccess;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (!e) l.smem = smem;
+      return e;
+    }
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (!e) limits.push_back({kern, dev, smem});
+  return e;
+}
 
 }  // namespace mp
 

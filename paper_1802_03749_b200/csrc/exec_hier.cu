@@ -249,13 +249,13 @@ mp_status launch_sched(const LoopView<T>& v, HierView H, const mp_hier_plan& P, 
     MP_FAIL(MP_ERR_CAPACITY, "a block needs %zu shared bytes, over the 232448-byte limit", smem);
   if (df) {
     auto kern = hier_block_kernel<Op, T, LAYOUT, true, SlotT, WSAME>;
-    MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MP_CUDA_TRY(raise_smem_limit(reinterpret_cast<const void*>(kern), smem));
     kern<<<P.num_blocks, threads, smem, st>>>(v, H);
     MP_CHECK_LAUNCH();
     return MP_OK;
   }
   auto kern = hier_block_kernel<Op, T, LAYOUT, false, SlotT, WSAME>;
-  MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MP_CUDA_TRY(raise_smem_limit(reinterpret_cast<const void*>(kern), smem));
   for (int c = 0; c < P.num_block_colours; ++c) {
     const int lo = P.colour_block_offsets_host[c], hi = P.colour_block_offsets_host[c + 1];
     if (hi <= lo) continue;

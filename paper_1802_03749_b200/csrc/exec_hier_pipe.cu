@@ -520,7 +520,7 @@ mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, b
   const int threads = consumers + 32;
   auto kern = dataflow ? hier_pipe_kernel<Op, T, LAYOUT, true, SlotT, PULL>
                        : hier_pipe_kernel<Op, T, LAYOUT, false, SlotT, PULL>;
-  MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MP_CUDA_TRY(raise_smem_limit(reinterpret_cast<const void*>(kern), smem));
   int per_sm = 0, dev = 0, sms = 0;
   MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   MP_CUDA_TRY(cudaGetDevice(&dev));

@@ -15,6 +15,11 @@ namespace mp {
 // thread-local message of the last failing call (mp_last_error)
 void set_error(const char* fmt, ...);
 void clear_error();
+// Raise a kernel's dynamic shared-memory limit to at least `smem` bytes on the
+// current device.  The limit only ever grows (process-wide, under a mutex), so
+// threads launching the same kernel with different sizes never lower it
+// between another thread's set and launch.
+cudaError_t raise_smem_limit(const void* kern, size_t smem);
 
 #define MP_CUDA_TRY(expr)                                                                 \
   do {                                                                                    \

@@ -251,7 +251,7 @@ extern "C" mp_status mp_plan_block_points(int32_t nb, const int32_t* block_offse
   int m = next_pow2(max_block * __builtin_popcount(mask) > 0 ? max_block * __builtin_popcount(mask) : 1);
   size_t smem = (size_t)m * 8;
   if (smem > 227 * 1024) MP_FAIL(MP_ERR_CAPACITY, "block of %d elements x %d slots too large to plan", max_block, arity);
-  MP_CUDA_TRY(cudaFuncSetAttribute(block_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MP_CUDA_TRY(raise_smem_limit(reinterpret_cast<const void*>(block_points_kernel), smem));
   block_points_kernel<<<nb, 256, smem, as_stream(stream)>>>(nb, block_offsets, map, n, arity, layout, mask, counts,
                                                             offsets, ids);
   MP_CHECK_LAUNCH();
@@ -272,7 +272,7 @@ extern "C" mp_status mp_plan_local_slots(int32_t nb, const int32_t* block_offset
   MP_CUDA_TRY(cudaMemcpyAsync(d_miss, &big, sizeof(int32_t), cudaMemcpyHostToDevice, st));
   // a staged list holds at most block_size x arity <= 8192 points
   const size_t smem = 8192 * sizeof(int32_t);
-  MP_CUDA_TRY(cudaFuncSetAttribute(local_slots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MP_CUDA_TRY(raise_smem_limit(reinterpret_cast<const void*>(local_slots_kernel), smem));
   local_slots_kernel<<<nb, 256, smem, st>>>(nb, block_offsets, map, n, arity, layout, mask, st_off, st_ids,
                                             local_slots, wr_off, wr_ids, written_slots, d_miss);
   MP_CHECK_LAUNCH();
@@ -297,7 +297,7 @@ extern "C" mp_status mp_plan_thread_colours(int32_t nb, const int32_t* block_off
   MP_CUDA_TRY(cudaMallocAsync(&d_over, sizeof(int32_t), st));
   int32_t big = INT_MAX;
   MP_CUDA_TRY(cudaMemcpyAsync(d_over, &big, sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  MP_CUDA_TRY(cudaFuncSetAttribute(thread_colour_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MP_CUDA_TRY(raise_smem_limit(reinterpret_cast<const void*>(thread_colour_kernel), smem));
   thread_colour_kernel<<<nb, 32, smem, st>>>(nb, block_offsets, map, n, arity, layout, mask, max_block, colours, counts,
                                              sorted_order, d_over);
   MP_CHECK_LAUNCH();

@@ -599,3 +599,36 @@ def test_captured_graph_replays_the_loop():
         assert bit_equal(a.tensors["res"].cpu().numpy(), b.tensors["res"].cpu().numpy()), sched
     with pytest.raises(mp.KernelSpecError):
         mp.bind(plan, kernel, schedule="stream-dataflow").capture()
+
+
+def test_concurrent_threads_with_different_plan_sizes():
+    """Threads launching the same executors with different shared-memory sizes
+    (different plans) at once: the per-kernel limit only grows, so no launch
+    sees a limit lowered by another thread (cudaErrorInvalidValue before)."""
+    import threading
+
+    errors = []
+    dims = [(60, 40), (90, 70), (40, 30), (120, 50)]
+
+    def worker(d, bs):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                mesh = mp.generate_mesh("quad2d", d, dtype="f64")
+                kernel = mp.kernel_for_mesh("flux", mesh)
+                plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps", block_size=bs))
+                loops = [mp.bind(plan, kernel, schedule=s) for s in ("pipelined", "pipelined-pull", "colour",
+                                                                      "stream", "stream-pull")]
+                for _ in range(20):
+                    for lp in loops:
+                        lp.run(torch.cuda.current_stream())
+                torch.cuda.current_stream().synchronize()
+        except Exception as exc:  # pragma: no cover - surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(d, bs)) for d, bs in zip(dims, (32, 64, 128, 96))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=300)
+    assert not errors, errors
