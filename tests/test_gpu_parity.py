@@ -599,6 +599,14 @@ def test_captured_graph_replays_the_loop():
         assert bit_equal(a.tensors["res"].cpu().numpy(), b.tensors["res"].cpu().numpy()), sched
     with pytest.raises(mp.KernelSpecError):
         mp.bind(plan, kernel, schedule="stream-dataflow").capture()
+    glob = mp.build_global_plan(mesh, kernel, mp.PlanConfig(strategy="global", reorder="gps"))
+    a, b = mp.bind(glob, kernel), mp.bind(glob, kernel)
+    g = b.capture()
+    a.run()
+    a.run()
+    g.replay()
+    torch.cuda.synchronize()
+    assert bit_equal(a.tensors["res"].cpu().numpy(), b.tensors["res"].cpu().numpy())
 
 
 def test_concurrent_threads_with_different_plan_sizes():
