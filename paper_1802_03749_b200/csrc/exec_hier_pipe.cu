@@ -157,9 +157,14 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
   if (!PULL)
     for (int i = threadIdx.x; i < H.max_staged * IC; i += nthreads) sh_inc[i] = T(0);
   __syncthreads();
+  // Programmatic dependent launch: the next colour's CTAs may start as this
+  // grid's retire; every access to the incremented array is ordered after the
+  // producer's griddepcontrol.wait (consumers only write rows it has filled).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------- producer -------------------------------
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // Descriptor batches + a K-deep staged-id ring keep every dependent load
     // (claim -> block id -> descriptor -> staged ids) many fills ahead of its
     // use: lane i of a batch resolves fill (base + i); the next batch is
@@ -536,14 +541,28 @@ mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, b
     MP_CHECK_LAUNCH();
     return MP_OK;
   }
+  static const bool no_pdl = getenv("MESHPLAN_NO_PDL") != nullptr;
+  bool first = true;
   for (int c = 0; c < P.num_block_colours; ++c) {
     const int lo = P.colour_block_offsets_host[c], hi = P.colour_block_offsets_host[c + 1];
     if (hi <= lo) continue;
     H.list = P.blocks_by_colour + lo;
     H.list_len = hi - lo;
     const int grid = (hi - lo) < resident ? (hi - lo) : resident;
-    kern<<<grid, threads, smem, st>>>(v, H);
-    MP_CHECK_LAUNCH();
+    // PDL only between the colour launches of this call (the first one may
+    // follow any other work on the stream)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (!first && !no_pdl) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, v, H));
+    first = false;
   }
   return MP_OK;
 }
