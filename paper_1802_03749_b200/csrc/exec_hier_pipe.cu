@@ -159,12 +159,13 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
   __syncthreads();
   // Programmatic dependent launch: the next colour's CTAs may start as this
   // grid's retire; every access to the incremented array is ordered after the
-  // producer's griddepcontrol.wait (consumers only write rows it has filled).
+  // producer's griddepcontrol.wait, issued before its first increment-row
+  // gather (consumers only write rows it has filled).
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------- producer -------------------------------
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    bool pdl_waited = false;  // griddepcontrol.wait before the first increment-row gather
     // Descriptor batches + a K-deep staged-id ring keep every dependent load
     // (claim -> block id -> descriptor -> staged ids) many fills ahead of its
     // use: lane i of a batch resolves fill (base + i); the next batch is
@@ -304,6 +305,10 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
       // tickets; the consumers never wait, so the smallest unfinished ticket
       // always progresses (all CTAs are co-resident).
       const bool inc_rows = true;
+      if (!pdl_waited) {  // descriptors, ids and map rows above are plan data
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        pdl_waited = true;
+      }
       if constexpr (DATAFLOW) {
         const int q0 = __ldg(H.pred_offsets + b), nq = __ldg(H.pred_offsets + b + 1) - q0;
         for (int i = lane; i < nq; i += 32) {
