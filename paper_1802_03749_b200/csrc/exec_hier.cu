@@ -28,6 +28,8 @@
 //    their duplicated staged / written rows hit L2 instead of HBM.  A ticket is
 //    only taken by a resident CTA and only waits on earlier tickets: no
 //    deadlock.  The increment rows are read after the wait (L2-only loads).
+#include <stdlib.h>
+
 #include "mp_loop.cuh"
 
 namespace mp {
@@ -126,8 +128,13 @@ __global__ void __launch_bounds__(1024) hier_block_kernel(LoopView<T> v, HierVie
   T* sh_a = reinterpret_cast<T*>(smem_raw);  // [ns][REG]: staged reads, then increments
   T* sh_r = sh_a + ns * REG;                 // [ns][IC]: increment rows (colour schedule)
 
-  // A. issue everything that does not depend on another block
+  // A. issue everything that does not depend on another block; then wait for
+  //    the previous colour launch (programmatic dependent launch: this grid
+  //    may start while it drains) before the first access to the incremented
+  //    array
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (stage) gather_rows<T, LAYOUT, (RC > 0 ? RC : 1)>(sh_a, v.ind, H.staged_ids + s0, ns, v.ind_comps, v.npts, tid, nt);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if constexpr (PREFETCH_INC) gather_rows<T, LAYOUT, IC>(sh_r, v.inc, H.staged_ids + s0, ns, IC, v.npts, tid, nt);
   asm volatile("cp.async.commit_group;" ::: "memory");
 
@@ -256,12 +263,26 @@ mp_status launch_sched(const LoopView<T>& v, HierView H, const mp_hier_plan& P, 
   }
   auto kern = hier_block_kernel<Op, T, LAYOUT, false, SlotT, WSAME>;
   MP_CUDA_TRY(raise_smem_limit(reinterpret_cast<const void*>(kern), smem));
+  static const bool no_pdl = getenv("MESHPLAN_NO_PDL") != nullptr;
+  bool first = true;
   for (int c = 0; c < P.num_block_colours; ++c) {
     const int lo = P.colour_block_offsets_host[c], hi = P.colour_block_offsets_host[c + 1];
     if (hi <= lo) continue;
     H.colour_base = lo;
-    kern<<<hi - lo, threads, smem, st>>>(v, H);
-    MP_CHECK_LAUNCH();
+    // PDL only between this call's colour launches (the first one may follow
+    // any other work on the stream)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(hi - lo);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (!first && !no_pdl) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, v, H));
+    first = false;
   }
   return MP_OK;
 }
