@@ -6,6 +6,8 @@
 // elements write a common point (checked by the planner / mp_race_check), so
 // the result equals the reference execute_global bit for bit:
 // init + sum over colours in colour order (simulator.py:382-418).
+#include <stdlib.h>
+
 #include "mp_loop.cuh"
 
 namespace mp {
@@ -13,6 +15,7 @@ namespace {
 
 template <class Op, typename T, int LAYOUT>
 __global__ void __launch_bounds__(256) global_colour_kernel(LoopView<T> v, int64_t lo, int64_t hi) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int64_t e = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= hi) return;
   int32_t p[Op::ARITY];
@@ -29,6 +32,9 @@ __global__ void __launch_bounds__(256) global_colour_kernel(LoopView<T> v, int64
   load_direct<Op, T>(v, e, d);
   T o[Op::ARITY][Op::IC];
   compute<Op, T>(v, r, d, o);
+  // the previous colour launch (programmatic dependent launch) must be done
+  // before the increment rows are read
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // slot order matters only for repeated points within one row (np.add.at order)
 #pragma unroll
   for (int s = 0; s < Op::ARITY; ++s)
@@ -47,15 +53,27 @@ mp_status launch_global(const mp_loop& L, const int64_t* offsets, int32_t ncol, 
     mp_status s = check_loop_shape(L, Op::ARITY, Op::RC, Op::DC, Op::IC);
     if (s) return s;
     LoopView<T> v = make_view<T>(L);
+    static const bool no_pdl = getenv("MESHPLAN_NO_PDL") != nullptr;
+    bool first = true;
     for (int c = 0; c < ncol; ++c) {
       int64_t lo = offsets[c], hi = offsets[c + 1];
       if (hi <= lo) continue;
       int64_t nblk = (hi - lo + bs - 1) / bs;
+      // PDL between this call's colour launches only (as the hierarchical executors)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)nblk);
+      cfg.blockDim = dim3(bs);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = (!first && !no_pdl) ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
       if (L.ind_layout == MP_AOS)
-        global_colour_kernel<Op, T, MP_AOS><<<(unsigned)nblk, bs, 0, st>>>(v, lo, hi);
+        MP_CUDA_TRY(cudaLaunchKernelEx(&cfg, global_colour_kernel<Op, T, MP_AOS>, v, lo, hi));
       else
-        global_colour_kernel<Op, T, MP_SOA><<<(unsigned)nblk, bs, 0, st>>>(v, lo, hi);
-      MP_CHECK_LAUNCH();
+        MP_CUDA_TRY(cudaLaunchKernelEx(&cfg, global_colour_kernel<Op, T, MP_SOA>, v, lo, hi));
+      first = false;
     }
     return MP_OK;
   }
