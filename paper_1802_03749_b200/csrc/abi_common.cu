@@ -48,6 +48,54 @@ cudaError_t raise_smem_limit(const void* kern, size_t smem) {
   return e;
 }
 
+namespace {
+struct DfChain {
+  int dev;
+  cudaEvent_t last;
+  bool armed;
+};
+std::mutex g_df_mu;
+std::vector<DfChain> g_df;
+DfChain* df_chain(int dev) {
+  for (auto& c : g_df)
+    if (c.dev == dev) return &c;
+  g_df.push_back({dev, nullptr, false});
+  return &g_df.back();
+}
+}  // namespace
+
+// The mutex is held from begin to end, so a launch from another host thread
+// cannot slip between this launch's wait and its record.
+cudaError_t static_dataflow_begin(cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  g_df_mu.lock();
+  DfChain* c = df_chain(dev);
+  if (!c->last) {
+    e = cudaEventCreateWithFlags(&c->last, cudaEventDisableTiming);
+    if (e) {
+      g_df_mu.unlock();
+      return e;
+    }
+  }
+  e = c->armed ? cudaStreamWaitEvent(st, c->last, 0) : cudaSuccess;
+  if (e) g_df_mu.unlock();
+  return e;
+}
+
+cudaError_t static_dataflow_end(cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (!e) {
+    DfChain* c = df_chain(dev);
+    e = cudaEventRecord(c->last, st);
+    if (!e) c->armed = true;
+  }
+  g_df_mu.unlock();
+  return e;
+}
+
 }  // namespace mp
 
 extern "C" const char* mp_last_error(void) { return mp::last_error(); }

@@ -542,8 +542,11 @@ mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, b
     H.list = P.order;
     H.list_len = P.num_blocks;
     const int grid = P.num_blocks < resident ? P.num_blocks : resident;
+    MP_CUDA_TRY(static_dataflow_begin(st));  // static claims: never co-resident with another such grid
     kern<<<grid, threads, smem, st>>>(v, H);
-    MP_CHECK_LAUNCH();
+    const cudaError_t le = cudaGetLastError();
+    MP_CUDA_TRY(static_dataflow_end(st));
+    MP_CUDA_TRY(le);
     return MP_OK;
   }
   static const bool no_pdl = getenv("MESHPLAN_NO_PDL") != nullptr;

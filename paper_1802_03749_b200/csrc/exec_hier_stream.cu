@@ -53,7 +53,9 @@
 // smaller tickets; the CTA holding the smallest unfinished ticket has
 // finished all its earlier ones, and sync warps keep releasing finished
 // blocks while they poll, so that ticket always progresses while every CTA
-// is resident (the grid is capped at the occupancy-derived resident count).
+// is resident (the grid is capped at the occupancy-derived resident count,
+// and static-claim dataflow grids on a device are chained one after another,
+// mp_common.cuh static_dataflow_begin).
 // An opt-in variant (MESHPLAN_STREAM_TMA=1) gathers read rows with TMA
 // tile::gather4 into per-stage mbarriers (measured slower).
 #include <cuda.h>
@@ -899,7 +901,10 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
     H.pred_pad = P.tpred_pad;
     H.ntickets = P.num_blocks;
     const int grid = P.num_blocks < resident ? P.num_blocks : resident;
-    MP_CUDA_TRY(launch_pdl(kern, grid, threads, smem, st, false, v, H, qmap));
+    MP_CUDA_TRY(static_dataflow_begin(st));
+    const cudaError_t le = launch_pdl(kern, grid, threads, smem, st, false, v, H, qmap);
+    MP_CUDA_TRY(static_dataflow_end(st));
+    MP_CUDA_TRY(le);
     return MP_OK;
   }
   bool first = true;

@@ -20,6 +20,15 @@ void clear_error();
 // threads launching the same kernel with different sizes never lower it
 // between another thread's set and launch.
 cudaError_t raise_smem_limit(const void* kern, size_t smem);
+// Static-claim dataflow grids (fill f of CTA c takes ticket c + f*grid; CTAs
+// spin on predecessor flags) are deadlock-free only while all their CTAs are
+// resident.  A non-spinning grid sharing the GPU only delays residency; a
+// second spinning static-claim grid can hold the SMs the first one's
+// unscheduled CTAs need.  Every such launch on a device is therefore chained
+// behind the previous one (process-wide event chain): call begin before and
+// end after the launch, on the launch stream.
+cudaError_t static_dataflow_begin(cudaStream_t st);
+cudaError_t static_dataflow_end(cudaStream_t st);
 
 #define MP_CUDA_TRY(expr)                                                                 \
   do {                                                                                    \

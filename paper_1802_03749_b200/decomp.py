@@ -212,7 +212,7 @@ def slab_bounds(nx: int, ny: int, world: int):
 class DistributedLoop:
     """One rank's share of a decomposed flux-type loop: local plan + halo."""
 
-    def __init__(self, mesh_local, kernel, dec: Decomposition, transport, config, schedule="dataflow",
+    def __init__(self, mesh_local, kernel, dec: Decomposition, transport, config, schedule="stream",
                  overlap=None):
         import paper_1802_03749_b200 as mp
 

@@ -169,10 +169,22 @@ class DeviceLoop:
     kernel: KernelSpec
     tensors: dict
     loop: _native.MpLoop
-    schedule: int = _native.MP_SCHED_DATAFLOW
+    schedule: int = _native.MP_SCHED_COLOUR
     pipelined: bool | str = False  # True: warp-specialised kernel, "stream": streamed kernel
     launches: int = 0
     _keep: list = field(default_factory=list)
+    # dataflow schedules: this loop's own epoch-stamped block flags and ticket
+    # counters (the plan stays immutable, so plans run concurrently),
+    # the plan struct pointing at them, and the event of this loop's last
+    # execution (executions of one loop are chained: they share the flags)
+    _df_struct: object = None
+    _df_state: tuple = ()
+    epoch: int = 0
+    _df_event: object = None
+
+    def _dataflow(self) -> bool:
+        return (not isinstance(self.plan, GlobalPlan) and self.pipelined not in ("atomic", "temp-array")
+                and self.schedule & 3 == _native.MP_SCHED_DATAFLOW)
 
     def run(self, stream=None, sub=None) -> None:
         """Launch one full execution of the loop (all colours); asynchronous.
@@ -198,11 +210,18 @@ class DeviceLoop:
             _native.call("mp_exec_global", self.loop, offs.ctypes.data, len(offs) - 1,
                          int(self.plan.config.block_size), sp)
         else:
-            if self.schedule & 3 == _native.MP_SCHED_DATAFLOW:
-                dp.epoch = dp.epoch % 0xFFFFFFFF + 1  # flags hold the last epoch; never 0
             fn = ("mp_exec_hier_stream" if self.pipelined == "stream" else
                   "mp_exec_hier_pipelined" if self.pipelined else "mp_exec_hier")
-            _native.call(fn, self.loop, dp.struct_cached(), self.schedule, max(dp.epoch, 1), sp)
+            if not self._dataflow():
+                _native.call(fn, self.loop, dp.struct_cached(), self.schedule, 1, sp)
+                return
+            cur = stream if stream is not None else torch.cuda.current_stream()
+            if self._df_event is not None:
+                cur.wait_event(self._df_event)  # the previous execution released these flags
+            self.epoch = self.epoch % 0xFFFFFFFF + 1  # flags hold the last epoch; never 0
+            _native.call(fn, self.loop, self._df_struct, self.schedule, self.epoch, sp)
+            self._df_event = torch.cuda.Event()
+            self._df_event.record(cur)
 
     def capture(self):
         """One execution captured as a CUDA graph (colour schedules: the
@@ -210,13 +229,20 @@ class DeviceLoop:
         submission).  Returns the ``torch.cuda.CUDAGraph``; ``replay()`` runs
         the loop on the current stream's device.  Dataflow schedules stamp a
         fresh epoch per execution and are not capturable."""
-        if self.schedule & 3 == _native.MP_SCHED_DATAFLOW and not isinstance(self.plan, GlobalPlan):
+        if self._dataflow():
             raise KernelSpecError("dataflow schedules take a new epoch per execution; capture a colour schedule")
+        # warm-up outside the capture (kernel attributes, occupancy queries),
+        # with the incremented array restored afterwards: capturing has no
+        # effect on the bound arrays
+        inc = next(a.array for a in self.kernel.args if a.mode == "increment")
+        saved = self.tensors[inc].clone()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            self.run(side)  # warm: kernel attributes and occupancy queries happen outside the capture
+            self.run(side)
+            self.tensors[inc].copy_(saved)
         torch.cuda.current_stream().wait_stream(side)
+        del saved
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             self.run(torch.cuda.current_stream())
@@ -255,7 +281,7 @@ class DeviceLoop:
             return n * (2 if self.pipelined == "temp-array" else 1)
         if isinstance(self.plan, GlobalPlan):
             return int(np.count_nonzero(np.diff(self.plan._device.colour_offsets)))
-        if self.schedule & 3 == _native.MP_SCHED_DATAFLOW:
+        if self._dataflow():
             return 1 if self.plan.num_blocks else 0
         return int(np.count_nonzero(np.diff(self.plan._device.colour_block_offsets)))
 
@@ -305,9 +331,15 @@ def _array_tensor(arr: DataArray, dev) -> torch.Tensor:
     return host.to(dev, non_blocking=True)
 
 
-def bind(plan, kernel: KernelSpec, tensors: dict | None = None, schedule: str = "dataflow") -> DeviceLoop:
+def bind(plan, kernel: KernelSpec, tensors: dict | None = None, schedule: str = "stream") -> DeviceLoop:
     """Bind ``kernel`` to ``plan``; ``tensors`` (name -> device tensor in plan
-    numbering and plan layout) default to uploads of ``plan.mesh``."""
+    numbering and plan layout) default to uploads of ``plan.mesh``.
+
+    ``schedule`` picks the executor (``SCHEDULES``); the default ``"stream"``
+    is the streamed colour-schedule kernel, the fastest on every config.
+    Dataflow schedules get their own flags and tickets per bound loop, so any
+    number of loops may run one plan at once; executions of one loop are
+    ordered after each other on the device."""
     if kernel.signature_key() != plan.kernel_key:
         raise KernelSpecError("plan was built for a different kernel signature")
     mesh = plan.mesh
@@ -348,7 +380,16 @@ def bind(plan, kernel: KernelSpec, tensors: dict | None = None, schedule: str = 
         temp = torch.empty(max(m.from_set.size * m.arity * inc_arr.components, 1),
                            dtype=TORCH_DTYPES[inc_arr.elem_type], device=dev)
         keep = [off, refs, temp]
-    return DeviceLoop(plan, kernel, t, L, sched, pipelined, _keep=keep)
+    loop = DeviceLoop(plan, kernel, t, L, sched, pipelined, _keep=keep)
+    if loop._dataflow():
+        nb = max(plan.num_blocks, 1)
+        flags = torch.zeros(nb, dtype=torch.int32, device=dev)
+        tickets = torch.zeros(2, dtype=torch.int32, device=dev)
+        base = plan._device.struct_cached()
+        st = type(base).from_buffer_copy(base)
+        st.flags, st.tickets = flags.data_ptr(), tickets.data_ptr()
+        loop._df_struct, loop._df_state = st, (flags, tickets)
+    return loop
 
 
 # ------------------------------------------------------------------------------
@@ -506,7 +547,7 @@ def _report(plan, kernel, loop: DeviceLoop, ms: float | None) -> MetricsReport:
     )
 
 
-def _run_and_collect(plan, kernel, schedule="dataflow"):
+def _run_and_collect(plan, kernel, schedule="stream"):
     loop = bind(plan, kernel, schedule=schedule)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
@@ -527,10 +568,12 @@ def execute_global(plan: GlobalPlan, kernel: KernelSpec):
     return _run_and_collect(plan, kernel)
 
 
-def execute_hierarchical(plan: HierarchicalPlan, kernel: KernelSpec, schedule: str = "dataflow"):
-    """Hierarchical shared-memory execution; ``schedule`` is ``"dataflow"``
-    (one launch, DAG-ordered blocks) or ``"colour"`` (one launch per block
-    colour, the paper's scheme).  Both give bit-identical results."""
+def execute_hierarchical(plan: HierarchicalPlan, kernel: KernelSpec, schedule: str = "stream"):
+    """Hierarchical shared-memory execution; ``schedule`` names an executor
+    of ``SCHEDULES``: ``"stream"`` (default; one launch per block colour, the
+    paper's scheme, persistent streamed kernel), ``"colour"`` (CTA per block),
+    the ``"*-dataflow"`` forms (one launch, DAG-ordered blocks) and the
+    ``"*-pull"`` forms.  All give bit-identical results."""
     if not isinstance(plan, HierarchicalPlan):
         raise KernelSpecError("execute_hierarchical needs a HierarchicalPlan")
     return _run_and_collect(plan, kernel, schedule)

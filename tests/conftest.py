@@ -17,6 +17,17 @@ GOLDEN = REPO / "tests" / "golden"
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (runs on the B200 box)")
+    config.addinivalue_line("markers", "slow: full-size BASELINE configs (minutes; -m gpu runs them)")
+
+
+def pytest_collection_modifyitems(config, items):
+    """gpu-marked tests skip (instead of failing) on a host without CUDA."""
+    if has_gpu() or os.environ.get("MESHPLAN_FORCE_GPU_TESTS"):
+        return
+    skip = pytest.mark.skip(reason="needs a CUDA device")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
 
 
 def has_gpu() -> bool:

@@ -1,0 +1,202 @@
+"""Parity at the BASELINE config sizes (C1-C5, seed 0).
+
+``tests/golden/fingerprints.json`` holds CRC32 fingerprints of the REAL
+reference's plans and loop results at these sizes
+(``tests/golden/make_fingerprints.py``, run where /root/reference exists).
+Here, on the GPU:
+
+* every GPU-built plan (global / hierarchical x none / gps / partition) is
+  compared array by array with the reference planner's (plan.py:408-579);
+* every executor's result, restored to the original numbering, is compared
+  with the reference ``execute_serial`` (simulator.py:215-242) -- bit-exact,
+  the generator's 1/1024-grid data makes every sum exact;
+* on non-quantised random data (C1, C4 stand-in) the results are compared
+  bit for bit with the reference's own ``execute_global`` /
+  ``execute_hierarchical`` on the same plan (simulator.py:355, 525) and the
+  GPU ``execute_serial`` with the reference ``execute_serial``;
+* C1 and C2 are also compared with the oracle's serial loop (oracle/loops.py).
+
+C4 (23.9M faces) and C5 (64M edges) run the headline plans and schedules of
+``bench.py`` against the reference serial result (``slow``, still -m gpu).
+"""
+
+import json
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1802_03749_b200 as mp
+from conftest import GOLDEN, INC_OF
+
+pytestmark = pytest.mark.gpu
+
+FP = json.loads((GOLDEN / "fingerprints.json").read_text())
+HIER_SCHEDULES = ("stream", "stream-pull", "pipelined", "pipelined-pull", "colour", "stream-dataflow", "dataflow",
+                  "pipelined-dataflow")
+
+
+def crc(a) -> dict:
+    a = np.ascontiguousarray(a)
+    if a.dtype.kind in "iu":
+        a = a.astype("<i8")
+    return {"crc32": zlib.crc32(a.tobytes()) & 0xFFFFFFFF, "len": int(a.size)}
+
+
+def plan_mismatches(plan, m, want: dict) -> list:
+    got = {"elem_fwd": crc(plan.set_perms[m.from_set.name].forward),
+           "point_fwd": crc(plan.set_perms[m.to_set.name].forward)}
+    if isinstance(plan, mp.GlobalPlan):
+        got["colours"] = crc(plan.colours.colours)
+        got["colour_offsets"] = [int(x) for x in plan.colour_offsets]
+        got["num_colours"] = int(plan.num_colours)
+    else:
+        ((_, (sp, sids)),) = plan.staged.items()
+        ((_, (wp, wids)),) = plan.written.items()
+        got.update(block_offsets=crc(plan.block_offsets), block_colours=crc(plan.block_colours.colours),
+                   num_block_colours=int(plan.block_colours.num_colours),
+                   block_colour_counts=[int(x) for x in plan.block_colours.counts],
+                   thread_colours=crc(plan.thread_colours), thread_colour_counts=crc(plan.thread_colour_counts),
+                   staged_ptr=crc(sp), staged_ids=crc(sids), written_ptr=crc(wp), written_ids=crc(wids),
+                   shared_bytes=crc(plan.shared_bytes), num_blocks=int(plan.num_blocks))
+        assert abs(mp.reuse_factor(plan) - want["reuse_factor"]) < 1e-12
+    return [k for k, v in got.items() if want[k] != v]
+
+
+def randomise(mesh):
+    """make_fingerprints.randomise: standard normals, rng seed 7, mesh.data order."""
+    rng = np.random.default_rng(7)
+    return mesh.with_data(*[mp.DataArray(a.name, a.set, a.components,
+                                         rng.standard_normal(a.values.size).astype(a.values.dtype), a.layout)
+                            for a in mesh.data.values()])
+
+
+def config_mesh(name, lean=False):
+    rec = FP[name]
+    arrays = mp.workloads.arrays_for_kernel(rec["kernel"]) if lean else None
+    mesh = mp.generate_mesh(rec["family"], tuple(rec["dims"]), seed=rec["seed"], dtype=rec["dtype"], arrays=arrays)
+    return rec, mesh, mp.kernel_for_mesh(rec["kernel"], mesh)
+
+
+def build(rec, mesh, kernel, key):
+    strategy, reorder = key.split("/")
+    cfg = mp.PlanConfig(strategy=strategy, reorder=reorder, layout=rec["layout"], staging=rec["staging"],
+                        block_size=rec["block_size"])
+    return (mp.build_global_plan if strategy == "global" else mp.build_hierarchical_plan)(mesh, kernel, cfg)
+
+
+def run_restored(plan, kernel, inc, schedule):
+    if isinstance(plan, mp.GlobalPlan):
+        res, _ = mp.execute_global(plan, kernel)
+    else:
+        res, _ = mp.execute_hierarchical(plan, kernel, schedule=schedule)
+    return np.ascontiguousarray(plan.restore_data(res).data[inc].view2d())
+
+
+PLAN_CASES = [(name, key) for name in ("C1", "C2", "C3", "C4s", "C5") if name in FP
+              for key in FP[name].get("plans", {})]
+
+
+@pytest.mark.parametrize("name,key", PLAN_CASES, ids=[f"{n}-{k}" for n, k in PLAN_CASES])
+def test_config_plan_and_loop_match_the_reference(name, key):
+    """GPU plan == reference plan (every array), and every executor on it ==
+    the reference execute_serial, at the config's full size."""
+    if name == "C5":
+        pytest.skip("C5 runs in test_c5_headline_plan_and_loop (slow)")
+    rec, mesh, kernel = config_mesh(name)
+    m = next(iter(mesh.mappings.values()))
+    plan = build(rec, mesh, kernel, key)
+    bad = plan_mismatches(plan, m, FP[name]["plans"][key])
+    assert not bad, f"{name} {key}: plan arrays differ from the reference: {bad}"
+    inc = INC_OF[rec["kernel"]]
+    for sched in (("-",) if key.startswith("global") else HIER_SCHEDULES):
+        got = run_restored(plan, kernel, inc, sched)
+        assert crc(got) == FP[name]["serial"], f"{name} {key} {sched}: result differs from the reference serial loop"
+
+
+RAND_CASES = [(name, key) for name in ("C1", "C4s") if name in FP
+              for key, p in FP[name].get("plans", {}).items() if "rand_exec" in p]
+
+
+@pytest.mark.parametrize("name,key", RAND_CASES, ids=[f"{n}-{k}" for n, k in RAND_CASES])
+def test_config_same_plan_bit_exact_on_random_data(name, key):
+    """Non-quantised data: every executor on the reference's plan (built here
+    on the GPU, fingerprint-equal) reproduces the reference executor's own
+    result bit for bit -- the per-point colour order is the reference's."""
+    rec, mesh, kernel = config_mesh(name)
+    rmesh = randomise(mesh)
+    m = next(iter(rmesh.mappings.values()))
+    plan = build(rec, rmesh, kernel, key)
+    assert not plan_mismatches(plan, m, FP[name]["plans"][key])
+    inc = INC_OF[rec["kernel"]]
+    want = FP[name]["plans"][key]["rand_exec"]
+    for sched in (("-",) if key.startswith("global") else HIER_SCHEDULES):
+        assert crc(run_restored(plan, kernel, inc, sched)) == want, f"{name} {key} {sched}"
+    serial = mp.execute_serial(rmesh, kernel)
+    assert crc(np.ascontiguousarray(serial.data[inc].view2d())) == FP[name]["rand_serial"]
+
+
+@pytest.mark.parametrize("name", [n for n in ("C1", "C2") if n in FP])
+def test_config_gpu_serial_equals_oracle(name):
+    """The GPU execute_serial and the oracle's serial loop agree bit for bit
+    at C1 / C2 size, and both equal the reference's fingerprint."""
+    from oracle import loops
+
+    rec, mesh, kernel = config_mesh(name)
+    inc = INC_OF[rec["kernel"]]
+    m = next(iter(mesh.mappings.values()))
+    read = {"flux": "q"}.get(rec["kernel"])
+    want = loops.serial_loop(rec["kernel"], m.table, mesh.data[read].view2d() if read else None,
+                             np.ascontiguousarray(mesh.data["w"].view2d()),
+                             np.ascontiguousarray(mesh.data[inc].view2d()))
+    got = np.ascontiguousarray(mp.execute_serial(mesh, kernel).data[inc].view2d())
+    assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+    assert crc(got) == FP[name]["serial"]
+
+
+# ---- full-size headline configs (bench.py's plans) ------------------------------------
+
+
+@pytest.mark.slow
+def test_c5_headline_plan_and_loop():
+    """C5 (quad2d 5657^2, 64M edges, flux f64): the bench's GPS plan equals
+    the reference's, and the bench schedules' results equal the reference
+    execute_serial; the global-colouring baseline too."""
+    if "C5" not in FP:
+        pytest.skip("no C5 fingerprint")
+    rec, mesh, kernel = config_mesh("C5", lean=True)
+    m = next(iter(mesh.mappings.values()))
+    inc = INC_OF[rec["kernel"]]
+    if "hier/gps" in FP["C5"].get("plans", {}):
+        plan = build(rec, mesh, kernel, "hier/gps")
+        bad = plan_mismatches(plan, m, FP["C5"]["plans"]["hier/gps"])
+        assert not bad, f"C5 hier/gps plan differs from the reference: {bad}"
+    else:
+        plan = build(rec, mesh, kernel, "hier/gps")
+    for sched in ("stream", "stream-pull", "pipelined"):
+        assert crc(run_restored(plan, kernel, inc, sched)) == FP["C5"]["serial"], sched
+    del plan
+    torch.cuda.empty_cache()
+    gplan = build(rec, mesh, kernel, "global/gps")
+    assert crc(run_restored(gplan, kernel, inc, "-")) == FP["C5"]["serial"], "global"
+
+
+@pytest.mark.slow
+def test_c4_headline_plan_and_loop():
+    """C4 (hex3d-faces 200^3, 23.9M faces, face-flux f64, increment-only): the
+    bench's k-way partition plan runs on its executors and equals the
+    reference execute_serial bit for bit; the 4x4x8 structured hex blocks too."""
+    if "C4" not in FP:
+        pytest.skip("no C4 fingerprint")
+    rec, mesh, kernel = config_mesh("C4", lean=True)
+    inc = INC_OF[rec["kernel"]]
+    plan = build(rec, mesh, kernel, "hier/partition")
+    for sched in ("pipelined-pull", "stream-pull", "stream"):
+        assert crc(run_restored(plan, kernel, inc, sched)) == FP["C4"]["serial"], sched
+    del plan
+    torch.cuda.empty_cache()
+    cfg = mp.PlanConfig(reorder="structured:4,4,8", layout="aos", staging=rec["staging"], block_size=480)
+    splan = mp.build_hierarchical_plan(mesh, kernel, cfg)
+    for sched in ("stream-pull", "stream"):
+        assert crc(run_restored(splan, kernel, inc, sched)) == FP["C4"]["serial"], sched

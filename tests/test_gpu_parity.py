@@ -590,8 +590,8 @@ def test_captured_graph_replays_the_loop():
     for sched in ("stream", "stream-pull", "pipelined", "colour"):
         a = mp.bind(plan, kernel, schedule=sched)
         b = mp.bind(plan, kernel, schedule=sched)
-        g = b.capture()  # runs b once (warm-up)
-        for _ in range(3):
+        g = b.capture()  # the warm-up run's increments are undone: capture has no effect
+        for _ in range(2):
             a.run()
         for _ in range(2):
             g.replay()
@@ -602,7 +602,6 @@ def test_captured_graph_replays_the_loop():
     glob = mp.build_global_plan(mesh, kernel, mp.PlanConfig(strategy="global", reorder="gps"))
     a, b = mp.bind(glob, kernel), mp.bind(glob, kernel)
     g = b.capture()
-    a.run()
     a.run()
     g.replay()
     torch.cuda.synchronize()
@@ -640,3 +639,84 @@ def test_concurrent_threads_with_different_plan_sizes():
     for th in threads:
         th.join(timeout=300)
     assert not errors, errors
+
+
+DATAFLOW_SCHEDULES = ("dataflow", "stream-dataflow", "pipelined-dataflow", "pipelined-dataflow-pull")
+
+
+def test_one_plan_runs_concurrently_on_every_schedule():
+    """a finished plan may be executed concurrently.  Loops bound
+    to ONE plan on every schedule -- the dataflow ones included, which keep
+    per-loop flags and tickets, and whose static-claim grids the library
+    chains so two are never co-resident -- run at once from several threads on
+    their own streams; every result equals the single-run colour schedule bit
+    for bit (random data: any ordering slip shows).  One dataflow loop driven
+    from two streams alternately is ordered by its own event chain."""
+    import threading
+
+    mesh = mp.generate_mesh("quad2d", (160, 150), dtype="f64")
+    rng = np.random.default_rng(5)
+    mesh = mesh.with_data(*[mp.DataArray(a.name, a.set, a.components, rng.standard_normal(a.values.size), a.layout)
+                            for a in mesh.data.values()])
+    kernel = mp.kernel_for_mesh("flux", mesh)
+    plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps", block_size=64))
+    reps = 6
+    ref = mp.bind(plan, kernel, schedule="colour")
+    for _ in range(reps):
+        ref.run()
+    torch.cuda.synchronize()
+    want = ref.tensors["res"].cpu().numpy()
+    errors, results = [], {}
+
+    def worker(sched, k):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                lp = mp.bind(plan, kernel, schedule=sched)
+                for _ in range(reps):
+                    lp.run(torch.cuda.current_stream())
+                torch.cuda.current_stream().synchronize()
+                results[(sched, k)] = lp.tensors["res"].cpu().numpy()
+        except Exception as exc:  # pragma: no cover - surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(s, k)) for k in range(2)
+               for s in DATAFLOW_SCHEDULES + ("stream", "colour", "pipelined-pull")]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=300)
+    assert not errors, errors
+    assert len(results) == len(threads)
+    for key, got in results.items():
+        assert bit_equal(got, want), key
+    # one dataflow loop, executions alternating between two streams
+    for sched in DATAFLOW_SCHEDULES:
+        lp = mp.bind(plan, kernel, schedule=sched)
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        for i in range(reps):
+            lp.run(streams[i % 2])
+        torch.cuda.synchronize()
+        assert bit_equal(lp.tensors["res"].cpu().numpy(), want), sched
+
+
+def test_host_stream_on_a_dataflow_schedule():
+    """mp.HostStream with depth 2 on the dataflow schedules: each step's
+    loop has its own flags and tickets, so steps in flight together are
+    exact (they used to share the plan's)."""
+    mesh = mp.generate_mesh("quad2d", (220, 130), dtype="f64")
+    kernel = mp.kernel_for_mesh("flux", mesh)
+    plan = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(reorder="gps"))
+    inputs = {a.array: plan.mesh.data[a.array].values for a in kernel.args}
+    ref = mp.bind(plan, kernel, schedule="stream")
+    ref.run()
+    torch.cuda.synchronize()
+    want = ref.tensors["res"].cpu().numpy()
+    for sched in DATAFLOW_SCHEDULES:
+        hs = mp.HostStream(plan, kernel, schedule=sched, depth=2)
+        outs = [torch.empty(want.size, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        for k in range(6):
+            hs.step(inputs, outs[k % 2])
+            if k % 2 == 1:
+                hs.synchronize()
+                assert all(bit_equal(o.numpy(), want) for o in outs), sched

@@ -94,3 +94,33 @@ def test_known_answers():
     assert plans.global_plan(np.array([[0, 1], [2, 3]]), 4, [0, 1])["colour_offsets"].tolist() == [0, 2]
     # stable colour sort [1,0,1,0] -> order [1,3,0,2] (test_colouring.py:122-125)
     assert np.argsort(np.array([1, 0, 1, 0]), kind="stable").tolist() == [1, 3, 0, 2]
+
+
+# ---- the oracle at the BASELINE config sizes ------------------------------------------
+
+
+def _fingerprints():
+    import json
+
+    from conftest import GOLDEN
+
+    return json.loads((GOLDEN / "fingerprints.json").read_text())
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_oracle_serial_matches_reference_at_config_size(name):
+    """The oracle's serial loop on the full C1 / C2 mesh (seed 0, the
+    package generator, bit-identical to the reference's) reproduces the
+    CRC32 of the reference execute_serial result (make_fingerprints.py)."""
+    import zlib
+
+    import paper_1802_03749_b200 as mp
+
+    rec = _fingerprints()[name]
+    mesh = mp.generate_mesh(rec["family"], tuple(rec["dims"]), seed=rec["seed"], dtype=rec["dtype"],
+                            arrays=mp.workloads.arrays_for_kernel(rec["kernel"]))
+    t, ind, d, inc = _arrays(mesh, rec["kernel"])
+    got = np.ascontiguousarray(loops.serial_loop(rec["kernel"], t, ind, d, inc))
+    assert got.shape[0] == rec["n_points"]
+    assert (zlib.crc32(got.tobytes()) & 0xFFFFFFFF) == rec["serial"]["crc32"]
+    assert float(np.abs(got).sum()) == rec["serial_abs_sum"]
