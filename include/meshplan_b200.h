@@ -275,6 +275,20 @@ mp_status mp_heavy_edge_matching_device(int32_t n, const int64_t* indptr, const 
 mp_status mp_bfs_levels(int32_t n, const int64_t* indptr, const int32_t* indices, int32_t start, int32_t* levels,
                         int32_t* ecc, int32_t* visited, void* stream);
 
+/* Host BFS with the reference's outputs (numpy_impl.py:114-131; replaces
+ * _accel.bfs_levels, reorder.py:101/106/127/131): levels[n] (-1 unreached),
+ * the FIFO visit queue[n] (first *tail entries valid) and *tail. */
+mp_status mp_bfs_levels_host(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t start,
+                             int64_t* levels, int64_t* queue, int64_t* tail);
+
+/* All unordered pairs within each CSR segment, as (min, max)
+ * (numpy_impl.py:231-259; replaces _accel.pairs_from_segments,
+ * reorder.py:78, colouring.py:138, partition.py:82).  Pair order is
+ * unspecified in the reference; here segment by segment, (i, j) position
+ * order.  us == NULL: only *num_pairs (the size) is written. */
+mp_status mp_pairs_from_segments(int64_t num_segments, const int64_t* seg_indptr, const int64_t* seg_values,
+                                 int64_t* us, int64_t* vs, int64_t* num_pairs);
+
 /* Block conflict DAG for the dataflow schedule: for every pair of blocks
  * writing a common point, an edge from the lower to the higher
  * (colour, id); order = blocks sorted by (key, id) where

@@ -21,6 +21,10 @@ MP_F64, MP_F32, MP_I64, MP_I32 = 0, 1, 2, 3
 MP_AOS, MP_SOA = 0, 1
 MP_SCHED_COLOUR, MP_SCHED_DATAFLOW, MP_SCHED_PULL = 0, 1, 4
 OPS = {"flux": 0, "flux-noread": 1, "scatter8": 2, "face-flux": 3, "face-flux-heavy": 4}
+#: per device op: (arity, indirect-read components consumed, direct components
+#: consumed, increment components) -- the functor shapes of csrc/mp_ops.cuh
+OP_SHAPES = {"flux": (2, 4, 1, 4), "flux-noread": (2, 0, 2, 4), "scatter8": (8, 0, 4, 3),
+             "face-flux": (2, 5, 1, 5), "face-flux-heavy": (2, 7, 2, 5)}
 DTYPES = {"f64": MP_F64, "f32": MP_F32, "i64": MP_I64, "i32": MP_I32}
 LAYOUTS = {"aos": MP_AOS, "soa": MP_SOA}
 
@@ -73,6 +77,8 @@ _SIGNATURES = {
     "mp_greedy_colour_adj": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "mp_smallest_last_order": (c_i32, [c_i64, c_vp, c_vp, c_vp]),
     "mp_bfs_levels": (c_i32, [c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "mp_bfs_levels_host": (c_i32, [c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "mp_pairs_from_segments": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mp_plan_block_dag": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "mp_heavy_edge_matching": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "mp_cut_weight": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),

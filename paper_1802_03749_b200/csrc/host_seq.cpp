@@ -524,3 +524,75 @@ extern "C" mp_status mp_initial_partition(int64_t n, const int64_t* indptr, cons
   }
   return MP_OK;
 }
+
+// numpy_impl.py:114-131 -- FIFO breadth-first search from `start`: levels
+// (-1 unreached), the visit queue (first *tail entries valid) and its tail.
+// The queue order follows the adjacency order, as the reference's does.
+extern "C" mp_status mp_bfs_levels_host(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t start,
+                                        int64_t* levels, int64_t* queue, int64_t* tail) {
+  mp::clear_error();
+  if (n <= 0 || start < 0 || start >= n) {
+    mp::set_error("start node %lld out of range 0..%lld", (long long)start, (long long)n - 1);
+    return MP_ERR_VALIDATION;
+  }
+  for (int64_t v = 0; v < n; ++v) levels[v] = -1;
+  levels[start] = 0;
+  queue[0] = start;
+  int64_t head = 0, t = 1;
+  while (head < t) {
+    const int64_t u = queue[head++];
+    for (int64_t j = indptr[u]; j < indptr[u + 1]; ++j) {
+      const int64_t v = indices[j];
+      if (levels[v] < 0) {
+        levels[v] = levels[u] + 1;
+        queue[t++] = v;
+      }
+    }
+  }
+  *tail = t;
+  return MP_OK;
+}
+
+// numpy_impl.py:231-259 -- every unordered pair inside each segment
+// seg_values[seg_indptr[s] .. seg_indptr[s+1]), as (min, max).  The reference
+// leaves the pair order unspecified; here segments come in order and, within
+// one, pairs in (i, j) position order.  With us == NULL only *num_pairs is
+// written (size query); otherwise us / vs must hold *num_pairs entries.
+extern "C" mp_status mp_pairs_from_segments(int64_t num_segments, const int64_t* seg_indptr, const int64_t* seg_values,
+                                            int64_t* us, int64_t* vs, int64_t* num_pairs) {
+  mp::clear_error();
+  if (num_segments < 0) {
+    mp::set_error("negative segment count");
+    return MP_ERR_VALIDATION;
+  }
+  int64_t total = 0;
+  for (int64_t s = 0; s < num_segments; ++s) {
+    const int64_t k = seg_indptr[s + 1] - seg_indptr[s];
+    if (k < 0) {
+      mp::set_error("segment %lld has negative length", (long long)s);
+      return MP_ERR_VALIDATION;
+    }
+    total += k * (k - 1) / 2;
+  }
+  if (!us) {
+    *num_pairs = total;
+    return MP_OK;
+  }
+  if (*num_pairs < total) {
+    mp::set_error("pair buffers hold %lld entries, %lld needed", (long long)*num_pairs, (long long)total);
+    return MP_ERR_VALIDATION;
+  }
+  int64_t o = 0;
+  for (int64_t s = 0; s < num_segments; ++s) {
+    const int64_t a = seg_indptr[s], z = seg_indptr[s + 1];
+    for (int64_t i = a; i < z; ++i)
+      for (int64_t j = i + 1; j < z; ++j) {
+        const int64_t x = seg_values[i], y = seg_values[j];
+        us[o] = x < y ? x : y;
+        vs[o] = x < y ? y : x;
+        ++o;
+      }
+  }
+  *num_pairs = total;
+  return MP_OK;
+}

@@ -113,6 +113,33 @@ def useful_bytes(kernel: KernelSpec, mesh: Mesh) -> int:
     return total
 
 
+def consumed_bytes(kernel: KernelSpec, mesh: Mesh) -> int:
+    """Unique bytes the loop must move: like ``useful_bytes`` but counting
+    only the components the element function consumes: flux
+    reads ``w[:, 0]`` of the two edge weights (bench_kernels.py:177),
+    face-flux 5 of the 28 ``state`` components and ``facew[:, 0]``
+    (bench_kernels.py:233), the heavy variant 7 and 2.  Every consumed
+    indirect row read once, incremented rows read and written once, 4-byte
+    mapping entries: the ideal the roofline fraction is taken against."""
+    op = (kernel.device_op or "").partition(":")[0]
+    if op not in _native.OP_SHAPES:
+        raise KernelSpecError(f"kernel {kernel.name!r} has no device functor")
+    _, rc, dc, ic = _native.OP_SHAPES[op]
+    total, seen = 0, set()
+    for a in kernel.args:
+        if a.array in seen:
+            continue
+        seen.add(a.array)
+        arr = mesh.data[a.array]
+        comps = ic if a.mode == "increment" else (rc if a.indirect else dc)
+        total += (2 if a.mode == "increment" else 1) * arr.set.size * min(comps, arr.components) * \
+            arr.values.dtype.itemsize
+    for name in kernel.mapping_names():
+        m = mesh.mappings[name]
+        total += m.from_set.size * m.arity * MAPPING_ENTRY_BYTES
+    return total
+
+
 def _alt_costs(kernel, mesh):
     n = mesh.sets[kernel.iter_set_name(mesh)].size
     tb = ops = 0
