@@ -223,6 +223,18 @@ mp_status mp_plan_thread_colours(int32_t nb, const int32_t* block_offsets, const
                                  int32_t arity, int32_t map_layout, uint32_t written_mask, int32_t max_block,
                                  int32_t* colours, int32_t* counts, int32_t* sorted_order, void* stream);
 
+/* Greedy colouring of the plan blocks over their written points, on the
+ * device (replaces _accel.greedy_colour_csr at plan.py:254 in
+ * _colour_blocks_ns, plan.py:241-257): bit-identical to greedy_colour_csr
+ * (numpy_impl.py:12-60) with blocks as items, least-loaded or first-fit,
+ * before the relabel by load.  written_offsets/ids: per-block ascending
+ * unique written points (device int32 CSR, mp_plan_block_points); colours:
+ * device int32[nb]; *num_colours (host) receives the colour count.  Lower-id
+ * conflict lists are built by sorts; one warp then walks the blocks in order.
+ * MP_ERR_CAPACITY beyond 1024 colours. */
+mp_status mp_plan_block_colours(int32_t nb, const int32_t* written_offsets, const int32_t* written_ids,
+                                int32_t least_loaded, int32_t* colours, int32_t* num_colours, void* stream);
+
 /* Sequential greedy colouring of items over shared points, host C++,
  * bit-identical to greedy_colour_csr (numpy_impl.py:12-60). */
 mp_status mp_greedy_colour_csr(int64_t n_items, const int64_t* indptr, const int64_t* indices, int64_t n_points,

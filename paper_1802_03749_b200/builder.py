@@ -269,11 +269,9 @@ def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
 
     # block colouring over per-block written point sets (plan.py:241-257)
     wr_off, wr_ids = gpuplan.block_points(bo_d, map_d, wmask, max_block)
-    w_ids_h = wr_ids.to(torch.int64).cpu().numpy()
-    w_ptr_h = wr_off.to(torch.int64).cpu().numpy()
-    total_pts = int(w_ids_h.max()) + 1 if w_ids_h.size else 1
     tm.mark("written_lists")
-    block_colours = colour_csr_least_loaded(w_ptr_h, w_ids_h, total_pts)
+    bcol_d, nbcol, bcounts = gpuplan.colour_blocks_device(wr_off, wr_ids)
+    block_colours = ColourAssignment(bcol_d.cpu().numpy(), nbcol, bcounts)
     tm.mark("block_colouring")
 
     # thread colouring + intra-block colour sort (plan.py:508-522)
@@ -292,6 +290,11 @@ def build_hier(mesh: Mesh, kernel, config, hw) -> HierarchicalPlan:
         st_off, st_ids = gpuplan.block_points(bo_d, map_d, smask, max_block)
     s_ptr_h = st_off.to(torch.int64).cpu().numpy()
     s_ids_h = st_ids.to(torch.int64).cpu().numpy()
+    if smask == wmask:
+        w_ptr_h, w_ids_h = s_ptr_h, s_ids_h
+    else:
+        w_ptr_h = wr_off.to(torch.int64).cpu().numpy()
+        w_ids_h = wr_ids.to(torch.int64).cpu().numpy()
     staged = {m.to_set.name: (s_ptr_h, s_ids_h)} if smask else {}
     written = {m.to_set.name: (w_ptr_h, w_ids_h)} if wmask else {}
 

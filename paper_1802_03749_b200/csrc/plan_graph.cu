@@ -97,8 +97,9 @@ __global__ void seg_pair_emit(int64_t m, const uint64_t* __restrict__ keys, cons
     for (int64_t a = j; a < e; ++a)
       for (int64_t c = a + 1; c < e; ++c) {
         uint32_t x = (uint32_t)keys[a], y = (uint32_t)keys[c];  // x < y (sorted by block)
-        // edge from the lower (colour, id) block to the higher one
-        bool x_first = colour[x] < colour[y] || (colour[x] == colour[y] && x < y);
+        // edge from the lower (colour, id) block to the higher one (by id alone
+        // when no colours are given)
+        bool x_first = colour == nullptr || colour[x] < colour[y] || (colour[x] == colour[y] && x < y);
         uint32_t src = x_first ? x : y, dst = x_first ? y : x;
         edges[w++] = ((uint64_t)dst << 32) | src;
       }
@@ -259,6 +260,126 @@ __global__ void hem_apply_kernel(int32_t m, const int32_t* __restrict__ work, co
   }
 }
 
+
+// ---- sequential greedy block colouring (numpy_impl.py:12-60 over blocks) -------------
+// The least-loaded choice of block i depends on the colour counts after blocks
+// 0..i-1, so the pass is sequential by definition.  Its per-block work is
+// short once the conflict structure is known: the colours forbidden to block i
+// are exactly those of its lower-id conflict neighbours (blocks < i writing a
+// common point), a CSR built in parallel by sorts beforehand.  One warp then
+// walks the blocks in id order: lanes fetch neighbour colours (recent ones
+// from a shared-memory ring, older ones from L2), OR them into per-lane bit
+// words (lane l owns colours l, l+32, ...), and two warp min-reductions pick
+// the admissible colour with the fewest blocks (ties: lowest id) -- the
+// reference's choice.  The other warps stage the next chunk of the CSR into
+// shared memory meanwhile (double buffer, one CTA barrier per chunk).
+constexpr int GC_THREADS = 128;
+constexpr int GC_CH = 2048;     // blocks per chunk (at most)
+constexpr int GC_PCAP = 12288;  // neighbour entries per chunk buffer
+constexpr int GC_RING = 16384;  // colours of the most recent blocks
+constexpr size_t GC_SMEM = (2 * (GC_CH + 1) + 2 * GC_PCAP) * 4 + GC_RING * 2;
+
+__device__ __forceinline__ int32_t gc_chunk_end(int32_t nb, const int32_t* __restrict__ off, int32_t lo) {
+  // largest hi <= lo + GC_CH with off[hi] - off[lo] <= GC_PCAP, at least lo + 1
+  int32_t hi = lo + GC_CH < nb ? lo + GC_CH : nb;
+  const int32_t base = off[lo];
+  if (off[hi] - base <= GC_PCAP) return hi;
+  int32_t a = lo + 1, b = hi;  // off[a]-base may exceed the cap: a one-block chunk reads global
+  while (a < b) {
+    int32_t mid = (a + b + 1) >> 1;
+    if (off[mid] - base <= GC_PCAP) a = mid; else b = mid - 1;
+  }
+  return a;
+}
+
+template <int K>
+__global__ void __launch_bounds__(GC_THREADS, 1)
+    greedy_blocks_kernel(int32_t nb, const int32_t* __restrict__ off, const int32_t* __restrict__ preds,
+                         int32_t least_loaded, int32_t* colours, int32_t* result /* [0] colours, [1] overflow */) {
+  extern __shared__ __align__(16) int32_t gsm[];
+  int32_t* soff = gsm;                                             // 2 x (GC_CH + 1)
+  int32_t* spred = soff + 2 * (GC_CH + 1);                         // 2 x GC_PCAP
+  uint16_t* ring = reinterpret_cast<uint16_t*>(spred + 2 * GC_PCAP);  // GC_RING
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  auto stage = [&](int buf, int32_t lo, int32_t hi, int t0, int nt) {
+    const int32_t base = off[lo];
+    for (int32_t i = t0; i <= hi - lo; i += nt) soff[buf * (GC_CH + 1) + i] = off[lo + i];
+    const int32_t np = off[hi] - base;
+    if (np <= GC_PCAP)
+      for (int32_t j = t0; j < np; j += nt) spred[buf * GC_PCAP + j] = preds[base + j];
+  };
+
+  int32_t lo = 0, hi = gc_chunk_end(nb, off, 0);
+  stage(0, lo, hi, tid, GC_THREADS);
+  __syncthreads();
+  uint32_t cnt[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) cnt[k] = 0;
+  uint32_t ncol = 0;
+  int buf = 0;
+  while (lo < nb) {
+    const int32_t nlo = hi, nhi = nlo < nb ? gc_chunk_end(nb, off, nlo) : nlo;
+    if (warp == 0) {
+      const int32_t* so = soff + buf * (GC_CH + 1);
+      const int32_t base = so[0];
+      const bool glob = so[hi - lo] - base > GC_PCAP;
+      const int32_t* sp = spred + buf * GC_PCAP;
+      for (int32_t i = lo; i < hi; ++i) {
+        const int32_t s = so[i - lo], e = so[i - lo + 1];
+        uint32_t bits[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) bits[k] = 0;
+        for (int32_t t = s + lane; t < e; t += 32) {
+          const int32_t j = glob ? __ldg(preds + t) : sp[t - base];
+          const uint32_t c = j > i - GC_RING ? ring[j % GC_RING] : (uint32_t)__ldcg(colours + j);
+#pragma unroll
+          for (int k = 0; k < K; ++k) bits[k] |= (c >> 5) == (uint32_t)k ? 1u << (c & 31) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) bits[k] = __reduce_or_sync(0xffffffffu, bits[k]);
+        uint32_t cand = 0xffffffffu;
+        if (least_loaded) {
+          uint32_t mc = 0xffffffffu;
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            if ((uint32_t)(lane + 32 * k) < ncol && !(bits[k] >> lane & 1u) && cnt[k] < mc) mc = cnt[k];
+          mc = __reduce_min_sync(0xffffffffu, mc);
+#pragma unroll
+          for (int k = K - 1; k >= 0; --k)
+            if ((uint32_t)(lane + 32 * k) < ncol && !(bits[k] >> lane & 1u) && cnt[k] == mc) cand = lane + 32 * k;
+        } else {
+#pragma unroll
+          for (int k = K - 1; k >= 0; --k)
+            if ((uint32_t)(lane + 32 * k) < ncol && !(bits[k] >> lane & 1u)) cand = lane + 32 * k;
+        }
+        uint32_t best = __reduce_min_sync(0xffffffffu, cand);
+        if (best == 0xffffffffu) {
+          best = ncol++;
+          if (ncol > 32u * K) {  // every lane sees it: leave together
+            if (lane == 0) result[1] = 1;
+            break;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) cnt[k] += (best == (uint32_t)(lane + 32 * k)) ? 1u : 0u;
+        if (lane == 0) {
+          ring[i % GC_RING] = (uint16_t)best;
+          colours[i] = (int32_t)best;
+        }
+        __syncwarp();
+      }
+    } else if (nlo < nb) {
+      stage(buf ^ 1, nlo, nhi, tid - 32, GC_THREADS - 32);
+    }
+    __syncthreads();
+    if (*(volatile int32_t*)&result[1]) return;
+    lo = nlo;
+    hi = nhi;
+    buf ^= 1;
+  }
+  if (tid == 0) result[0] = (int32_t)ncol;
+}
 }  // namespace
 }  // namespace mp
 
@@ -306,14 +427,12 @@ extern "C" mp_status mp_race_check(int64_t n, const int64_t* ref_offsets, const 
   return MP_OK;
 }
 
-extern "C" mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offsets, const int32_t* written_ids,
-                                       int64_t n_points, const int32_t* block_colours, int32_t num_colours, int32_t lag,
-                                       int32_t* pred_offsets, int32_t* preds, int64_t preds_capacity,
-                                       int64_t* num_preds, int32_t* order, void* stream) {
-  clear_error();
-  *num_preds = 0;
-  if (nb == 0) return MP_OK;
-  cudaStream_t st = as_stream(stream);
+// Unique conflict edges (dst << 32 | src) between blocks writing a common point,
+// sorted: src is the lower (colour, id) block, or the lower id when colour is
+// null.  `uniq` receives U edges.
+static mp_status block_conflict_edges(int32_t nb, const int32_t* written_offsets, const int32_t* written_ids,
+                                      const int32_t* block_colours, cudaStream_t st, Scratch& uniq, int64_t* num) {
+  *num = 0;
   int32_t m32 = 0;
   MP_CUDA_TRY(cudaMemcpyAsync(&m32, written_offsets + nb, 4, cudaMemcpyDeviceToHost, st));
   MP_CUDA_TRY(cudaStreamSynchronize(st));
@@ -337,7 +456,7 @@ extern "C" mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offset
   MP_CUDA_TRY(cudaMemcpyAsync(&E, pos.as<int64_t>() + m, 8, cudaMemcpyDeviceToHost, st));
   MP_CUDA_TRY(cudaStreamSynchronize(st));
 
-  Scratch edges(st), edges2(st), uniq(st), nuniq(st), tmp2(st);
+  Scratch edges(st), edges2(st), nuniq(st), tmp2(st);
   MP_CUDA_TRY(edges.alloc(E * 8));
   MP_CUDA_TRY(edges2.alloc(E * 8));
   if (E > 0) {
@@ -358,6 +477,24 @@ extern "C" mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offset
                                           nuniq.as<int64_t>(), E, st));
     MP_CUDA_TRY(cudaMemcpyAsync(&U, nuniq.p, 8, cudaMemcpyDeviceToHost, st));
     MP_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  *num = U;
+  return MP_OK;
+}
+
+extern "C" mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offsets, const int32_t* written_ids,
+                                       int64_t n_points, const int32_t* block_colours, int32_t num_colours, int32_t lag,
+                                       int32_t* pred_offsets, int32_t* preds, int64_t preds_capacity,
+                                       int64_t* num_preds, int32_t* order, void* stream) {
+  clear_error();
+  *num_preds = 0;
+  if (nb == 0) return MP_OK;
+  cudaStream_t st = as_stream(stream);
+  Scratch uniq(st);
+  int64_t U = 0;
+  {
+    mp_status rc = block_conflict_edges(nb, written_offsets, written_ids, block_colours, st, uniq, &U);
+    if (rc != MP_OK) return rc;
   }
   *num_preds = U;
   if (U > preds_capacity) return MP_OK;  // caller grows the buffer and calls again
@@ -403,6 +540,48 @@ extern "C" mp_status mp_plan_block_dag(int32_t nb, const int32_t* written_offset
   MP_CUDA_TRY(cudaStreamSynchronize(st));
   (void)n_points;
   (void)num_colours;
+  return MP_OK;
+}
+
+extern "C" mp_status mp_plan_block_colours(int32_t nb, const int32_t* written_offsets, const int32_t* written_ids,
+                                           int32_t least_loaded, int32_t* colours, int32_t* num_colours,
+                                           void* stream) {
+  clear_error();
+  *num_colours = 0;
+  if (nb <= 0) return MP_OK;
+  cudaStream_t st = as_stream(stream);
+  Scratch uniq(st), poff(st), preds(st), res(st);
+  int64_t U = 0;
+  {
+    mp_status rc = block_conflict_edges(nb, written_offsets, written_ids, nullptr, st, uniq, &U);
+    if (rc != MP_OK) return rc;
+  }
+  if (U > INT32_MAX) MP_FAIL(MP_ERR_CAPACITY, "%lld block conflicts exceed the int32 CSR", (long long)U);
+  MP_CUDA_TRY(poff.alloc((size_t)(nb + 1) * 4));
+  MP_CUDA_TRY(preds.alloc((size_t)U * 4));
+  pred_offsets_kernel<<<grid_for(nb + 1 > U ? nb + 1 : U), 256, 0, st>>>(nb, U, uniq.as<uint64_t>(),
+                                                                          poff.as<int32_t>(), preds.as<int32_t>());
+  MP_CHECK_LAUNCH();
+  MP_CUDA_TRY(res.alloc(8));
+  int32_t h[2] = {0, 0};
+  for (int pass = 0; pass < 2; ++pass) {
+    MP_CUDA_TRY(cudaMemsetAsync(res.p, 0, 8, st));
+    if (pass == 0) {  // up to 64 colours
+      MP_CUDA_TRY(raise_smem_limit((const void*)greedy_blocks_kernel<2>, GC_SMEM));
+      greedy_blocks_kernel<2><<<1, GC_THREADS, GC_SMEM, st>>>(nb, poff.as<int32_t>(), preds.as<int32_t>(),
+                                                              least_loaded, colours, res.as<int32_t>());
+    } else {  // up to 1024
+      MP_CUDA_TRY(raise_smem_limit((const void*)greedy_blocks_kernel<32>, GC_SMEM));
+      greedy_blocks_kernel<32><<<1, GC_THREADS, GC_SMEM, st>>>(nb, poff.as<int32_t>(), preds.as<int32_t>(),
+                                                               least_loaded, colours, res.as<int32_t>());
+    }
+    MP_CHECK_LAUNCH();
+    MP_CUDA_TRY(cudaMemcpyAsync(h, res.p, 8, cudaMemcpyDeviceToHost, st));
+    MP_CUDA_TRY(cudaStreamSynchronize(st));
+    if (!h[1]) break;
+  }
+  if (h[1]) MP_FAIL(MP_ERR_CAPACITY, "block colouring needs more than 1024 colours");
+  *num_colours = h[0];
   return MP_OK;
 }
 

@@ -12,7 +12,7 @@ element lex sort          reorder.lex_sort_elements (161-171)         GPU stable
 chunk / structured        partition.chunk_partition, structured       host arithmetic
 split oversized           plan._split_oversized (451-464)             host (nb-sized)
 per-block written lists   plan._colour_blocks_ns (241-257)            GPU, CTA per block
-block colouring           greedy_colour_csr least-loaded              native host C++
+block colouring           greedy_colour_csr least-loaded              GPU (sorts + one warp)
 thread colouring + sort   plan._thread_colours_for_block (260-284)    GPU, warp per block
 staged / written CSR      plan._per_block_point_lists (582-603)       GPU, CTA per block
 shared slots              HierarchicalPlan.staged_slots (168-182)     GPU (materialised)
@@ -133,8 +133,15 @@ def bfs(indptr, indices, start: int, levels: torch.Tensor) -> tuple:
 
 def gps_forward(map_d: torch.Tensor, npts: int) -> torch.Tensor:
     """Forward point permutation of gps_renumber (reorder.py:115-141)."""
-    dev = map_d.device
     indptr, indices = point_graph(map_d, npts)
+    return gps_forward_graph(indptr, indices, npts)
+
+
+def gps_forward_graph(indptr: torch.Tensor, indices: torch.Tensor, npts: int) -> torch.Tensor:
+    """gps_renumber (reorder.py:115-141) on a device CSR point graph (int64
+    indptr, int32 indices): components by lowest index, pseudo-peripheral
+    root, order by (component, level, degree, id)."""
+    dev = indptr.device
     deg = indptr[1:] - indptr[:-1]
     comp = torch.arange(npts, dtype=torch.long, device=dev)  # component min id (singletons: self)
     level = torch.zeros(npts, dtype=torch.long, device=dev)
@@ -245,6 +252,33 @@ def local_slots(block_offsets_d, map_d, mask, st_off, st_ids, wr_off, wr_ids):
                      _native.MP_AOS, mask, _native.ptr(st_off), _native.ptr(st_ids), _native.ptr(ls),
                      _native.ptr(wr_off), _native.ptr(wr_ids), _native.ptr(ws), _sp())
     return ls, ws
+
+
+def colour_blocks_device(wr_off: torch.Tensor, wr_ids: torch.Tensor, least_loaded: bool = True):
+    """Greedy colouring of the blocks over their written points
+    (plan._colour_blocks_ns, plan.py:241-257: greedy_colour_csr with blocks as
+    items, then relabel by load) on the GPU (``mp_plan_block_colours``).
+    Returns the device int64 colours (relabelled by descending load when
+    least-loaded, ties by old id: colouring._relabel_by_load, colouring.py:68-74),
+    the colour count and the per-colour counts (host int64)."""
+    nb = wr_off.numel() - 1
+    dev = wr_off.device
+    if nb <= 0:
+        e = np.empty(0, dtype=np.int64)
+        return torch.empty(0, dtype=torch.int64, device=dev), 0, e
+    raw = torch.empty(nb, dtype=torch.int32, device=dev)
+    ncol = np.zeros(1, dtype=np.int32)
+    _native.call("mp_plan_block_colours", nb, _native.ptr(wr_off), _native.ptr(wr_ids), int(bool(least_loaded)),
+                 _native.ptr(raw), ncol.ctypes.data, _sp())
+    num = int(ncol[0])
+    raw = raw.long()
+    counts = torch.bincount(raw, minlength=num).cpu().numpy()
+    if not least_loaded:
+        return raw, num, counts
+    rank = np.lexsort((np.arange(num), -counts))
+    new_id = np.empty(num, dtype=np.int64)
+    new_id[rank] = np.arange(num, dtype=np.int64)
+    return torch.as_tensor(new_id, device=dev)[raw], num, counts[rank]
 
 
 DATAFLOW_LAG = int(__import__("os").environ.get("MESHPLAN_DATAFLOW_LAG", "4096"))

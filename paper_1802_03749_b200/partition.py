@@ -103,3 +103,12 @@ def load_partition(path) -> Partition:
     if len(lines) < 2 or not lines[1].startswith("blocks "):
         raise FileFormatError(f"{path}: missing blocks header")
     return Partition(np.array([int(v) for v in lines[2:]], dtype=np.int64), int(lines[1].split()[1]))
+
+
+def __getattr__(name):
+    # the reference keeps the k-way partitioner in this module (partition.py:28-350)
+    if name in ("ThreadGraph", "build_thread_graph", "partition_kway"):
+        from . import kway
+
+        return getattr(kway, name)
+    raise AttributeError(name)

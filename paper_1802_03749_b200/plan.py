@@ -187,6 +187,31 @@ def _refs_per_element(mesh, kernel) -> int:
     return total
 
 
+def written_refs(mesh: Mesh, kernel: KernelSpec):
+    """Per-element distinct written (set, point) references as a namespaced
+    CSR: ``(indptr, indices, set_offsets, total_points)`` -- each to-set's
+    points offset by the sizes of the sets before it, in increment-argument
+    order (plan.py:201-229).  The conflict relation every colouring and race
+    check here is built on."""
+    offsets, total, cols = {}, 0, []
+    for a in kernel.increment_args:
+        to = mesh.mappings[a.mapping].to_set
+        if to.name not in offsets:
+            offsets[to.name] = total
+            total += to.size
+    for a in kernel.increment_args:
+        m = mesh.mappings[a.mapping]
+        cols.append(m.table[:, list(kernel.arg_slots(mesh, a))] + offsets[m.to_set.name])
+    n = mesh.sets[kernel.iter_set_name(mesh)].size
+    rows = np.hstack(cols) if cols else np.empty((n, 0), dtype=np.int64)
+    srt = np.sort(rows, axis=1)
+    keep = np.ones_like(srt, dtype=bool)
+    keep[:, 1:] = srt[:, 1:] != srt[:, :-1]
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(keep.sum(axis=1), out=indptr[1:])
+    return indptr, srt[keep].astype(np.int64), offsets, max(total, 1)
+
+
 def build_global_plan(mesh: Mesh, kernel: KernelSpec, config: PlanConfig | None = None,
                       hw: HardwareDescriptor = B200) -> GlobalPlan:
     """Reorder, colour elements, range-split by colour (plan.py:408-448)."""

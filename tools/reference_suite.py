@@ -1,0 +1,128 @@
+#!/usr/bin/env python
+"""Run the reference's OWN test suite against this package (drop-in check).
+
+``meshplan`` (and its submodules) are aliased to ``paper_1802_03749_b200``
+before pytest collects the reference's tests (pkg/tests), so every
+``import meshplan as mp`` / ``from meshplan.X import Y`` in them binds to
+this package -- GPU planner, sm_100a executors -- with the reference's
+assertions unchanged.  The tests come from ``baseline/_ref_tests`` (staged by
+tools/stage_reference.sh in the build container; git-ignored, travels to the
+GPU box) or ``--tests DIR``.
+
+Module map (reference -> here):
+
+    meshplan.bench_kernels -> workloads        meshplan.simulator -> executor
+    meshplan.reorder       -> reorder          meshplan.colouring -> colouring
+    meshplan.partition     -> partition (+kway) meshplan.plan      -> plan
+    meshplan._accel        -> accel            mesh, kernelspec, permutation,
+                                               structured, errors, hardware
+
+Out of scope, so their tests are deselected and
+listed with the reason in the summary: the CLI (``meshplan.cli``), text mesh
+I/O (``meshplan.meshio``), and the P100 transaction / occupancy cost model
+(``count_cache_lines``, ``wide_transfer_model``, ``colour_loop_efficiency``,
+MetricsReport transaction fields); the accel backend-equivalence file is run
+by tests/test_accel_seam.py instead.  Those names resolve to stubs that raise
+so that a module importing them still collects.
+
+    python tools/reference_suite.py [--tests DIR] [-- extra pytest args]
+"""
+
+import argparse
+import sys
+import types
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(REPO))
+
+OUT_OF_SCOPE_FILES = {
+    "test_cli.py": "reference CLI (out of scope)",
+    "test_meshio.py": "text mesh I/O (out of scope)",
+    "test_accel_backends.py": "run by tests/test_accel_seam.py (this backend in numba_impl's place)",
+}
+
+
+def _stub(name, why):
+    def f(*a, **k):
+        raise NotImplementedError(f"{name}: {why}")
+
+    f.__name__ = name
+    return f
+
+
+def install_alias():
+    import paper_1802_03749_b200 as pkg
+    from paper_1802_03749_b200 import (accel, colouring, errors, executor, hardware, kernelspec, kway, mesh, partition,
+                                       permutation, plan, reorder, structured, workloads)
+
+    cost = "P100 cost model (out of scope: measured ncu counters replace it)"
+    sim = types.ModuleType("meshplan.simulator")
+    sim.__dict__.update({k: v for k, v in vars(executor).items() if not k.startswith("__")})
+    for n in ("count_cache_lines", "wide_transfer_model", "colour_loop_efficiency"):
+        setattr(sim, n, _stub(n, cost))
+    part = types.ModuleType("meshplan.partition")
+    part.__dict__.update({k: v for k, v in vars(partition).items() if not k.startswith("__")})
+    for n in ("ThreadGraph", "build_thread_graph", "partition_kway"):
+        setattr(part, n, getattr(kway, n))
+    cli = types.ModuleType("meshplan.cli")
+    cli.main = _stub("main", "reference CLI (out of scope)")
+    mio = types.ModuleType("meshplan.meshio")
+    mio.read_mesh = _stub("read_mesh", "text mesh I/O (out of scope)")
+    mio.write_mesh = _stub("write_mesh", "text mesh I/O (out of scope)")
+    for n in ("count_cache_lines", "wide_transfer_model"):
+        if not hasattr(pkg, n):
+            setattr(pkg, n, getattr(sim, n))
+    for n in ("read_mesh", "write_mesh"):
+        if not hasattr(pkg, n):
+            setattr(pkg, n, getattr(mio, n))
+    mods = {
+        "meshplan": pkg, "meshplan.bench_kernels": workloads, "meshplan.simulator": sim,
+        "meshplan.reorder": reorder, "meshplan.colouring": colouring, "meshplan.partition": part,
+        "meshplan.plan": plan, "meshplan._accel": accel, "meshplan.mesh": mesh, "meshplan.kernelspec": kernelspec,
+        "meshplan.permutation": permutation, "meshplan.structured": structured, "meshplan.errors": errors,
+        "meshplan.hardware": hardware, "meshplan.cli": cli, "meshplan.meshio": mio,
+    }
+    for k, v in mods.items():
+        sys.modules[k] = v
+    for k, v in mods.items():
+        if "." in k:
+            setattr(pkg, k.split(".", 1)[1], v) if not hasattr(pkg, k.split(".", 1)[1]) else None
+    pkg.simulator = sim
+    pkg.partition = part
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tests", default=str(REPO / "baseline" / "_ref_tests"))
+    ap.add_argument("--deselect-file", default=str(REPO / "tools" / "reference_suite_deselect.txt"))
+    ap.add_argument("rest", nargs="*")
+    args = ap.parse_args()
+    tests = Path(args.tests)
+    if not tests.is_dir():
+        print(f"reference tests not staged at {tests} (run tools/stage_reference.sh in the build container)")
+        return 2
+    install_alias()
+    import pytest
+
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, str(tests))
+    pargs = [str(tests), "-q", "-p", "no:cacheprovider", "-o", "addopts=", "--rootdir", str(tests),
+             "-W", "ignore::DeprecationWarning"]
+    for f, why in OUT_OF_SCOPE_FILES.items():
+        pargs += ["--ignore", str(tests / f)]
+        print(f"ignored {f}: {why}")
+    dfile = Path(args.deselect_file)
+    if dfile.exists():
+        for line in dfile.read_text().splitlines():
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            node, _, why = line.partition("  # ")
+            pargs += ["--deselect", str(tests / node.strip())]
+            print(f"deselected {node.strip()}: {why}")
+    return pytest.main(pargs + list(args.rest))
+
+
+if __name__ == "__main__":
+    sys.exit(main())
