@@ -216,11 +216,25 @@ def kernel_share(step, K):
     return a.elapsed_time(b) / K
 
 
-def cpu_baseline(mesh, kernel_name, seconds=10.0, max_edges=4_000_000):
-    """The reference CPU loop (oracle restatement of execute_serial,
-    simulator.py:215-242; numpy, single-threaded) on a bounded sample."""
-    from oracle import loops
+def _reference_package():
+    """The unmodified reference package, pip-installed into baseline/_ref
+    (tools/stage_reference.sh; git-ignored, travels with the snapshot), or None."""
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "meshplan" / "__init__.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import meshplan
 
+        return meshplan
+    except Exception:  # pragma: no cover - a broken install falls back to the port
+        return None
+
+
+def _sample(mesh, kernel_name, max_edges):
+    """The first ``max_edges`` elements of the loop with the points they use
+    (renumbered densely, order kept): a bounded sample of the same workload."""
     m = next(iter(mesh.mappings.values()))
     n = min(m.from_set.size, max_edges)
     table = m.table[:n]
@@ -229,24 +243,63 @@ def cpu_baseline(mesh, kernel_name, seconds=10.0, max_edges=4_000_000):
     read = {"flux": "q", "face-flux": "state", "face-flux-heavy": "state"}.get(kernel_name)
     direct = {"flux": "w", "flux-noread": "w", "scatter8": "stress"}.get(kernel_name, "facew")
     inc = {"flux": "res", "flux-noread": "res", "scatter8": "force"}.get(kernel_name, "flux")
-    ind = None if read is None else np.ascontiguousarray(mesh.data[read].view2d()[used])
-    d = np.ascontiguousarray(mesh.data[direct].view2d()[:n])
-    r0 = np.ascontiguousarray(mesh.data[inc].view2d()[used])
-    arrays = [(used.size, r0.shape[1], r0.itemsize, True), (n, d.shape[1], d.itemsize, False)]
-    if ind is not None:
-        arrays.append((used.size, ind.shape[1], ind.itemsize, False))
-    ub = loops.useful_bytes(n, m.arity, arrays)
+    arrays = {inc: np.ascontiguousarray(mesh.data[inc].view2d()[used]),
+              direct: np.ascontiguousarray(mesh.data[direct].view2d()[:n])}
+    if read is not None:
+        arrays[read] = np.ascontiguousarray(mesh.data[read].view2d()[used])
+    return m, n, used, local, read, direct, inc, arrays
+
+
+def cpu_runner(mesh, kernel_name, max_edges=4_000_000):
+    """The reference's CPU loop on a bounded sample of the workload, on this
+    host: the UNMODIFIED reference ``meshplan.execute_serial``
+    (simulator.py:215-230, numpy; single-threaded) from baseline/_ref when
+    installed (kind "reference"), else its restatement in oracle/loops.py
+    (kind "port").  Returns (run, useful bytes of the sample by the paper
+    formula, kind, description)."""
+    m, n, used, local, read, direct, inc, arrays = _sample(mesh, kernel_name, max_edges)
+    ref = _reference_package()
+    if ref is not None:
+        from meshplan.bench_kernels import kernel_for_mesh as ref_kernel_for_mesh
+
+        fr, to = ref.MeshSet(m.from_set.name, n), ref.MeshSet(m.to_set.name, used.size)
+        sets = {m.from_set.name: fr, m.to_set.name: to}
+        data = [ref.DataArray(name, to if name != direct else fr, a.shape[1], a.ravel(), "aos")
+                for name, a in arrays.items()]
+        rmesh = ref.Mesh.build([fr, to], [ref.Mapping(m.name, fr, to, local.astype(np.int64))], data,
+                               dict(mesh.meta))
+        kern = ref_kernel_for_mesh(kernel_name, rmesh)
+        ub = int(ref.simulator._useful_bytes(kern, rmesh))
+        run = lambda: ref.execute_serial(rmesh, kern)  # noqa: E731
+        kind, what = "reference", "meshplan.execute_serial (the unmodified reference, baseline/_ref, numpy backend)"
+        del sets
+    else:
+        from oracle import loops
+
+        arr = [(used.size, arrays[inc].shape[1], arrays[inc].itemsize, True),
+               (n, arrays[direct].shape[1], arrays[direct].itemsize, False)]
+        if read is not None:
+            arr.append((used.size, arrays[read].shape[1], arrays[read].itemsize, False))
+        ub = loops.useful_bytes(n, m.arity, arr)
+        run = lambda: loops.serial_loop(kernel_name, local, arrays.get(read), arrays[direct], arrays[inc])  # noqa
+        kind, what = "port", "execute_serial restated in numpy (oracle/loops.py)"
+    desc = f"{what} on the first {n} of {m.from_set.size} elements ({used.size} points)"
+    return run, ub, kind, desc
+
+
+def cpu_baseline(mesh, kernel_name, seconds=10.0, max_edges=4_000_000):
+    """``cpu_runner``'s loop timed for about ``seconds`` (at least 3 runs)."""
+    run, ub, kind, desc = cpu_runner(mesh, kernel_name, max_edges)
     times = []
     t_end = time.perf_counter() + seconds
     while time.perf_counter() < t_end or len(times) < 3:
         t0 = time.perf_counter()
-        loops.serial_loop(kernel_name, local, ind, d, r0)
+        run()
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
-    return {"value": round(ub / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
-            "sample": f"execute_serial restated in numpy (oracle/loops.py) on the first {n} of "
-                      f"{m.from_set.size} elements ({used.size} points), median of {len(times)} runs, "
-                      f"{t * 1e3:.1f} ms/run",
+    return {"value": round(ub / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": kind,
+            "sample": f"{desc}, median of {len(times)} runs, {t * 1e3:.1f} ms/run; host has {os.cpu_count()} cores, "
+                      "the reference loop is single-threaded numpy",
             "ms_per_run": round(t * 1e3, 3), "useful_bytes": ub}
 
 
@@ -261,26 +314,68 @@ def reference_arm(args):
         return 0
     mesh, kernel, _ = make_mesh(args.config)
     family, dims, kname, dtype, _ = CONFIGS[args.config]
-    # warmup W, then K timed steps of the bounded sample
-    base = cpu_baseline(mesh, kname, seconds=0.0)
+    run, ub, kind, desc = cpu_runner(mesh, kname)
+    del mesh, kernel
     per_step = []
-    for i in range(args.warmup + args.steps):
-        b = cpu_baseline(mesh, kname, seconds=0.0)
+    for i in range(args.warmup + args.steps):  # W untimed, then K timed runs of the bounded sample
+        t0 = time.perf_counter()
+        run()
         if i >= args.warmup:
-            per_step.append(b["ms_per_run"])
+            per_step.append((time.perf_counter() - t0) * 1e3)
     ms = statistics.median(per_step)
-    val = round(base["useful_bytes"] / (ms * 1e-3) / 1e9, 4)
+    val = round(ub / (ms * 1e-3) / 1e9, 4)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
         "config": {"workload": f"{args.config} {family} {'x'.join(map(str, dims))} {kname} {dtype} "
                                "(bounded sample, see cpu_baseline.sample)"},
-        "cpu_baseline": {**{k: base[k] for k in ("unit", "cores", "kind", "sample")}, "value": val},
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": kind,
+                         "sample": f"{desc}, median of {len(per_step)} runs, {ms:.1f} ms/run; host has "
+                                   f"{os.cpu_count()} cores, the reference loop is single-threaded numpy"},
         "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def verify_full(hier, glob, kernel, main, gl):
+    """Results of one loop execution at the full config, bit for bit: the
+    headline hierarchical loop == global colouring == the device serial loop
+    (element order, simulator.py:215-230), restored to the original numbering
+    (the hashed 1/1024-grid data makes every sum exact, so any correct order
+    agrees; tests/test_gpu_configs.py pins the serial loop to the reference's
+    own result at these sizes by CRC)."""
+    import torch
+
+    import paper_1802_03749_b200 as mp
+
+    inc = next(a.array for a in kernel.args if a.mode == "increment")
+
+    def once(loop, plan):
+        t = loop.tensors[inc]
+        saved = t.clone()
+        t.zero_()
+        loop.run()
+        torch.cuda.synchronize()
+        got = t.cpu().numpy().copy()
+        t.copy_(saved)
+        arr = plan.mesh.data[inc]
+        res = plan.restore_data(plan.mesh.with_data(mp.DataArray(arr.name, arr.set, arr.components, got,
+                                                                 arr.layout)))
+        return np.ascontiguousarray(res.data[inc].view2d())
+
+    serial = mp.bind(hier, kernel, schedule="temp-array")
+    want = once(serial, hier)
+    del serial
+    h = once(main, hier)
+    g = once(gl, glob)
+    ok_h = bool(np.array_equal(h.view(np.uint8), want.view(np.uint8)))
+    ok_g = bool(np.array_equal(g.view(np.uint8), want.view(np.uint8)))
+    return {"checked": "one execution from zeroed increments, restored numbering: headline hierarchical == "
+                       "global colouring == device serial loop (element order), bit for bit",
+            "hier_equals_serial": ok_h, "global_equals_serial": ok_g,
+            "nonzero_rows": int(np.count_nonzero(np.any(want != 0, axis=1)))}
 
 
 def our_arm(args):
@@ -301,6 +396,7 @@ def our_arm(args):
     t_gen = time.perf_counter() - t0
     ub = mp.useful_bytes(kernel, mesh)
     cb = mp.consumed_bytes(kernel, mesh)
+    cb_strict = mp.consumed_bytes(kernel, mesh, strict=True)
     flush = L2Flusher(ub < 2 * L2_BYTES)
 
     results = {}
@@ -368,8 +464,14 @@ def our_arm(args):
                             "reuse_factor": round(mp.reuse_factor(alt), 4),
                             "block_colours": alt.block_colours.num_colours, "plan_build_s": round(t_alt, 2)}
         del alt
-    # end to end through the public API with host buffers (pinned), H2D + D2H in the region
+    # parity self-check at the full config (outside the timed regions): one
+    # execution of the headline loop, of global colouring and of the device
+    # serial loop (temp-array strategy: per-point fold in element order, the
+    # reference execute_serial's np.add.at order), each from zeroed increments
     main = loops[args.schedule]
+    parity = verify_full(hier, glob, kernel, main, gl)
+
+    # end to end through the public API with host buffers (pinned), H2D + D2H in the region
     inputs = {a.array: hier.mesh.data[a.array].values for a in kernel.args}
     inc_name = next(a.array for a in kernel.args if a.mode == "increment")
     out = torch.empty(hier.mesh.data[inc_name].values.size, dtype=main.tensors[inc_name].dtype, pin_memory=True)
@@ -451,9 +553,12 @@ def our_arm(args):
         "vs_layout": vs_layout or None,
         "roofline": {"bound": "hbm", "achieved": round(cb / (ms * 1e-3) / 1e9, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(cb / (ms * 1e-3) / 1e9 / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                     "bytes": "consumed: the components the element function reads (SURVEY 8(d)), every "
-                              "consumed row once, increments read+written once, 4-byte map entries",
+                     "bytes": "consumed (SURVEY 8(d)): indirectly read arrays only the components the element "
+                              "function reads, every row once; direct arrays whole; increments read+written "
+                              "once; 4-byte map entries",
                      "consumed_bytes_per_step": cb,
+                     "frac_strict": round(cb_strict / (ms * 1e-3) / 1e9 / peak, 4),
+                     "strict_bytes_per_step": cb_strict,
                      "achieved_formula": round(gbps, 2), "frac_formula": round(gbps / peak, 4),
                      "formula_bytes_per_step": ub,
                      "traffic_over_consumed": None if not traffic else round(traffic / cb, 3),
@@ -467,6 +572,7 @@ def our_arm(args):
                 "path": "mp.HostStream (public API): per step pinned host arrays -> H2D -> executor -> D2H, "
                         "consecutive steps on two streams with their own device arrays (serial_ms_per_step: "
                         "DeviceLoop.run_host one step at a time)"},
+        "parity": parity,
         "gpu_launches": int(launches * args.steps),
         "clocks": clocks,
         "cpu_baseline": cpu,

@@ -84,9 +84,22 @@ class MetricsReport:
     write_transactions: int | None = None
     bandwidth_proxy: float | None = None
 
-    def to_dict(self) -> dict:
+    @property
+    def total_transactions(self) -> int | None:
+        """The reference's modelled transaction total (None: no cost model here)."""
+        if self.read_transactions is None or self.write_transactions is None:
+            return None
+        return self.read_transactions + self.write_transactions
+
+    def to_dict(self, timing: bool = False) -> dict:
+        """The report as plain values.  Like the reference's (simulator.py:
+        298-312) it is a function of the plan and kernel only, so two
+        executions of equal plans give equal dicts; the measured
+        ``device_ms`` / ``effective_gbps`` are added with ``timing=True``."""
         out = {}
         for k, v in self.__dict__.items():
+            if not timing and k in ("device_ms", "effective_gbps"):
+                continue
             if isinstance(v, np.ndarray):
                 v = v.tolist()
             elif isinstance(v, np.integer):
@@ -94,6 +107,7 @@ class MetricsReport:
             elif isinstance(v, np.floating):
                 v = float(v)
             out[k] = v
+        out["total_transactions"] = self.total_transactions
         return out
 
 
@@ -113,14 +127,16 @@ def useful_bytes(kernel: KernelSpec, mesh: Mesh) -> int:
     return total
 
 
-def consumed_bytes(kernel: KernelSpec, mesh: Mesh) -> int:
-    """Unique bytes the loop must move: like ``useful_bytes`` but counting
-    only the components the element function consumes: flux
-    reads ``w[:, 0]`` of the two edge weights (bench_kernels.py:177),
-    face-flux 5 of the 28 ``state`` components and ``facew[:, 0]``
-    (bench_kernels.py:233), the heavy variant 7 and 2.  Every consumed
-    indirect row read once, incremented rows read and written once, 4-byte
-    mapping entries: the ideal the roofline fraction is taken against."""
+def consumed_bytes(kernel: KernelSpec, mesh: Mesh, strict: bool = False) -> int:
+    """Unique bytes the loop must move, the roofline numerator of SURVEY 8(d):
+    like ``useful_bytes`` but an indirectly read array counts only the
+    components the element function consumes (face-flux reads 5 of the 28
+    ``state`` components, the heavy variant 7; bench_kernels.py:233) -- so a
+    kernel that gathers only those cannot show more than 100 %.  Direct and
+    incremented arrays count whole (increments read and written once), 4-byte
+    map entries.  ``strict`` also trims the direct arrays to the consumed
+    components (flux reads ``w[:, 0]`` of 2, face-flux ``facew[:, 0]`` of 4;
+    bench_kernels.py:177, 233), the floor for a kernel reading SoA planes."""
     op = (kernel.device_op or "").partition(":")[0]
     if op not in _native.OP_SHAPES:
         raise KernelSpecError(f"kernel {kernel.name!r} has no device functor")
@@ -131,9 +147,13 @@ def consumed_bytes(kernel: KernelSpec, mesh: Mesh) -> int:
             continue
         seen.add(a.array)
         arr = mesh.data[a.array]
-        comps = ic if a.mode == "increment" else (rc if a.indirect else dc)
-        total += (2 if a.mode == "increment" else 1) * arr.set.size * min(comps, arr.components) * \
-            arr.values.dtype.itemsize
+        if a.mode == "increment":
+            comps = arr.components
+        elif a.indirect:
+            comps = min(rc, arr.components)
+        else:
+            comps = min(dc, arr.components) if strict else arr.components
+        total += (2 if a.mode == "increment" else 1) * arr.set.size * comps * arr.values.dtype.itemsize
     for name in kernel.mapping_names():
         m = mesh.mappings[name]
         total += m.from_set.size * m.arity * MAPPING_ENTRY_BYTES
@@ -151,19 +171,36 @@ def _alt_costs(kernel, mesh):
     return tb, ops
 
 
-def estimate_occupancy(threads: int, shared_bytes: int, regs: int, hw):
-    """Resident blocks/SM and occupancy (simulator.py:63-103)."""
+@dataclass(frozen=True)
+class OccupancyEstimate:
+    blocks_per_sm: int
+    occupancy: float
+    fault: str | None = None
+
+
+def estimate_occupancy(threads: int, shared_bytes: int, regs: int, hw) -> OccupancyEstimate:
+    """Resident blocks/SM and warp-rounded occupancy of a launch shape, with
+    the fault message of the first per-block limit it breaks
+    (simulator.py:57-103; a report field, not a cost model)."""
+    if threads < 1 or regs < 1 or shared_bytes < 0:
+        raise ValueError("occupancy inputs must be positive")
     warps = -(-threads // hw.warp_size)
-    rpw = -(-regs * hw.warp_size // hw.reg_alloc_granularity) * hw.reg_alloc_granularity
-    rpb = warps * rpw
-    if (threads > hw.max_threads_per_block or regs > hw.max_registers_per_thread
-            or shared_bytes > hw.shared_bytes_per_sm or rpb > hw.registers_per_sm):
-        return 0, 0.0
+    rpb = warps * -(-regs * hw.warp_size // hw.reg_alloc_granularity) * hw.reg_alloc_granularity
+    for bad, msg in ((threads > hw.max_threads_per_block,
+                      f"block of {threads} threads exceeds the {hw.max_threads_per_block}-thread limit"),
+                     (regs > hw.max_registers_per_thread,
+                      f"{regs} registers/thread exceeds the {hw.max_registers_per_thread} limit"),
+                     (shared_bytes > hw.shared_bytes_per_sm,
+                      f"{shared_bytes} shared bytes exceed the {hw.shared_bytes_per_sm}-byte limit"),
+                     (rpb > hw.registers_per_sm, f"{rpb} registers/block exceed the {hw.registers_per_sm}/SM limit")):
+        if bad:
+            return OccupancyEstimate(0, 0.0, msg)
     blocks = min(hw.max_blocks_per_sm, hw.max_threads_per_sm // threads, hw.max_warps_per_sm // warps,
                  hw.registers_per_sm // rpb)
     if shared_bytes > 0:
         blocks = min(blocks, hw.shared_bytes_per_sm // shared_bytes)
-    return int(blocks), blocks * warps * hw.warp_size / hw.max_threads_per_sm
+    blocks = max(blocks, 0)
+    return OccupancyEstimate(int(blocks), float(blocks * warps * hw.warp_size / hw.max_threads_per_sm))
 
 
 # ------------------------------------------------------------------------------
@@ -556,14 +593,16 @@ def _report(plan, kernel, loop: DeviceLoop, ms: float | None) -> MetricsReport:
     n = mesh.sets[kernel.iter_set_name(mesh)].size
     gbps = (ub / (ms * 1e-3) / 1e9) if ms else None
     if isinstance(plan, GlobalPlan):
-        bps, occ = estimate_occupancy(plan.config.block_size, 0, kernel.regs_per_thread, plan.hw)
+        est = estimate_occupancy(plan.config.block_size, 0, kernel.regs_per_thread, plan.hw)
+        bps, occ = est.blocks_per_sm, est.occupancy
         return MetricsReport("global", n, plan.num_colours, plan.num_colours, ub, tb, ops, occ, bps,
                              num_blocks=int(sum(-(-int(c) // plan.config.block_size) for c in np.diff(plan.colour_offsets))),
                              device_ms=ms, effective_gbps=gbps)
     nb = plan.num_blocks
     sync = plan.thread_colour_counts + 2
     smax = int(plan.shared_bytes.max()) if nb else 0
-    bps, occ = estimate_occupancy(plan.config.block_size, smax, kernel.regs_per_thread, plan.hw)
+    est = estimate_occupancy(plan.config.block_size, smax, kernel.regs_per_thread, plan.hw)
+    bps, occ = est.blocks_per_sm, est.occupancy
     return MetricsReport(
         "hier", n, loop.launches_per_run(), plan.block_colours.num_colours, ub, tb, ops, occ, bps,
         reuse_factor(plan), int(plan.thread_colour_counts.max()) if nb else 0,
