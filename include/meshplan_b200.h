@@ -191,6 +191,27 @@ mp_status mp_halo_pack(int32_t dtype, const void* src, const int32_t* rows, int6
 mp_status mp_halo_unpack(int32_t dtype, void* dst, const int32_t* rows, int64_t nrows, int32_t comps,
                          const void* src, int32_t mode, void* stream);
 
+/* Peer-memory halo exchange (graph-capturable, no NCCL on the data path).
+ * put: rows of src -> the receiver's mailbox slot (remote: an IPC-mapped or
+ * same-device pointer; slot = epoch parity, slot_elems apart), then
+ * *remote_flag = epoch once all stores are visible system-wide (done_counter:
+ * a zeroed device word private to this put).  get: wait until *flag reaches
+ * the epoch, then dst rows = (mode 0) / += (mode 1) the mailbox slot.  The
+ * epoch is read from device memory at kernel start; mp_epoch_bump adds 1. */
+mp_status mp_halo_put(int32_t dtype, const void* src, const int32_t* rows, int64_t nrows, int32_t comps, void* remote,
+                      int64_t slot_elems, uint32_t* remote_flag, const uint32_t* epoch, uint32_t* done_counter,
+                      void* stream);
+mp_status mp_halo_get(int32_t dtype, void* dst, const int32_t* rows, int64_t nrows, int32_t comps, const void* mailbox,
+                      int64_t slot_elems, const uint32_t* flag, const uint32_t* epoch, int32_t mode, void* stream);
+mp_status mp_epoch_bump(uint32_t* epoch, void* stream);
+/* Zeroed device allocation (cudaMalloc: IPC-exportable; free with mp_free),
+ * its 64-byte IPC handle, and a peer process's mapping of one (closed with
+ * mp_ipc_close). */
+mp_status mp_mailbox_alloc(int64_t bytes, void** ptr);
+mp_status mp_ipc_handle(void* ptr, unsigned char* handle);
+mp_status mp_ipc_open(const unsigned char* handle, void** ptr);
+mp_status mp_ipc_close(void* ptr);
+
 /* ---- race checks (simulator.py:245-261, 446-469) ---------------------------- */
 /* Keys (group*key_span + point) over every (element, written point) ref;
  * returns in first_pair[0..1] the first pair of distinct elements sharing a

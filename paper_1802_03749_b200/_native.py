@@ -90,6 +90,13 @@ _SIGNATURES = {
     "mp_initial_partition": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]),
     "mp_halo_pack":(c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "mp_halo_unpack": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp]),
+    "mp_halo_put": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "mp_halo_get": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp]),
+    "mp_epoch_bump": (c_i32, [c_vp, c_vp]),
+    "mp_mailbox_alloc": (c_i32, [c_i64, c_vp]),
+    "mp_ipc_handle": (c_i32, [c_vp, c_vp]),
+    "mp_ipc_open": (c_i32, [c_vp, c_vp]),
+    "mp_ipc_close": (c_i32, [c_vp]),
     "mp_free": (None, [c_vp]),
 }
 

@@ -24,6 +24,7 @@ on the generators' 1/1024-grid data and within reassociation tolerance
 otherwise.
 """
 
+import ctypes
 import queue
 from dataclasses import dataclass, field
 
@@ -200,6 +201,146 @@ class HaloExchange:
         return 2 * (len(self.halo) + len(self.exports)) + (1 if self.all_halo is not None else 0)
 
 
+# ---- peer-memory exchange (graph-capturable; no NCCL on the data path) ----------------
+
+
+class PeerHub:
+    """Mailbox registry of ranks running as threads of one process (one device
+    or several): a mailbox is published as its raw device pointer."""
+
+    def __init__(self):
+        self._boxes, self._cv = {}, __import__("threading").Condition()
+
+    def connector(self, rank: int):
+        def publish(ptr: int, layout: dict, needed) -> dict:
+            with self._cv:
+                self._boxes[rank] = (ptr, layout)
+                self._cv.notify_all()
+                if not self._cv.wait_for(lambda: all(p in self._boxes for p in needed), timeout=120):
+                    raise TimeoutError(f"rank {rank}: peers {sorted(set(needed) - set(self._boxes))} never published")
+                return {p: self._boxes[p] for p in needed}
+
+        publish.ipc = False
+        return publish
+
+
+def ipc_connector(allgather):
+    """Mailbox publication across processes: each rank shares the IPC handle
+    of its mailbox through ``allgather`` (e.g. torch.distributed
+    all_gather_object over the launcher's process group) and maps the
+    mailboxes of the peers it writes to (P2P over NVLink between devices)."""
+    def publish(ptr: int, layout: dict, needed) -> dict:
+        h = (ctypes.c_char * 64)()
+        _native.call("mp_ipc_handle", ptr, h)
+        everyone = allgather((bytes(h), layout))
+        out = {}
+        for p in needed:
+            handle, lay = everyone[p]
+            dptr = ctypes.c_void_p()
+            _native.call("mp_ipc_open", (ctypes.c_char * 64).from_buffer_copy(handle), ctypes.byref(dptr))
+            out[p] = (dptr.value, lay)
+        return out
+
+    publish.ipc = True
+    return publish
+
+
+class PeerExchange:
+    """Halo import / export through peer memory (SURVEY 8e step two).
+
+    Every rank owns one mailbox (``mp_mailbox_alloc``): two epoch-parity slots
+    per (peer, direction) it receives from, one flag per (peer, direction),
+    its put completion counters and its step epoch.  ``import_rows`` puts the
+    rows each peer imports straight into that peer's mailbox
+    (``mp_halo_put``: P2P stores, then a release of the epoch in the peer's
+    flag) and waits for / unpacks its own halo rows (``mp_halo_get``);
+    ``export_increments`` does the same for halo increments (added by the
+    owner) and re-zeroes the halo rows.  Nothing waits on the host, so a whole
+    step is capturable as a CUDA graph (``DistributedLoop.capture``).
+    ``publish(ptr, layout, needed)`` exchanges mailboxes (``PeerHub`` for
+    threads, ``ipc_connector`` for processes)."""
+
+    def __init__(self, dec: Decomposition, publish, device, dtype: torch.dtype, read_comps: int, inc_comps: int):
+        self.dec, self.dev, self.dtype = dec, torch.device(device), dtype
+        self.mp_dtype = TORCH_TO_MP[dtype]
+        item = torch.empty(0, dtype=dtype).element_size()
+        as_rows = lambda r: torch.as_tensor(np.asarray(r, dtype=np.int32), device=self.dev)  # noqa: E731
+        self.halo = {p: as_rows(r) for p, r in dec.halo_rows.items()}
+        self.exports = {p: as_rows(r) for p, r in dec.export_rows.items()}
+        self.all_halo = as_rows(np.concatenate(list(dec.halo_rows.values()))) if dec.halo_rows else None
+        self.rc, self.ic = read_comps, inc_comps
+        # layout (bytes): slots [2][rows*comps] per (dir, sender); flags [world][2]; counters [world][2]; epoch
+        layout, off = {}, 0
+        entries = [(("imp", p), len(r) * read_comps) for p, r in sorted(dec.halo_rows.items())] + \
+                  [(("exp", p), len(r) * inc_comps) for p, r in sorted(dec.export_rows.items())]
+        for (d, p), n in entries:
+            layout[f"{d}:{p}"] = (off, n)
+            off += 2 * max(n, 1) * item
+            off = (off + 255) & ~255
+        layout["flags"] = off
+        off += dec.world * 2 * 4
+        layout["counters"] = off
+        off += dec.world * 2 * 4
+        layout["epoch"] = off
+        off += 256
+        ptr = ctypes.c_void_p()
+        _native.call("mp_mailbox_alloc", off, ctypes.byref(ptr))
+        self.base, self.layout, self.bytes = ptr.value, layout, off
+        needed = sorted(set(dec.export_rows) | set(dec.halo_rows))
+        self.peers = publish(self.base, layout, needed)  # every rank takes part (a collective)
+        self._ipc = getattr(publish, "ipc", False)
+        self._opened = [v[0] for v in self.peers.values()] if self._ipc else []
+
+    def _flag(self, base: int, layout: dict, sender: int, d: int) -> int:
+        return base + layout["flags"] + (sender * 2 + d) * 4
+
+    @property
+    def epoch_ptr(self) -> int:
+        return self.base + self.layout["epoch"]
+
+    def bump(self) -> None:
+        _native.call("mp_epoch_bump", self.epoch_ptr, _native.stream_ptr())
+
+    def _put(self, arr, rows, comps, peer, d) -> None:
+        pbase, play = self.peers[peer]
+        off, n = play[f"{'imp' if d == 0 else 'exp'}:{self.dec.rank}"]
+        _native.call("mp_halo_put", self.mp_dtype, arr.data_ptr(), rows.data_ptr(), rows.numel(), comps, pbase + off, n,
+                     self._flag(pbase, play, self.dec.rank, d),
+                     self.epoch_ptr, self.base + self.layout["counters"] + (peer * 2 + d) * 4, _native.stream_ptr())
+
+    def _get(self, arr, rows, comps, peer, d, mode) -> None:
+        off, n = self.layout[f"{'imp' if d == 0 else 'exp'}:{peer}"]
+        _native.call("mp_halo_get", self.mp_dtype, arr.data_ptr(), rows.data_ptr(), rows.numel(), comps,
+                     self.base + off, n, self._flag(self.base, self.layout, peer, d), self.epoch_ptr, mode,
+                     _native.stream_ptr())
+
+    def import_rows(self, arr: torch.Tensor, comps: int) -> None:
+        for peer, rows in self.exports.items():
+            self._put(arr, rows, comps, peer, 0)
+        for peer, rows in self.halo.items():
+            self._get(arr, rows, comps, peer, 0, SET)
+
+    def export_increments(self, arr: torch.Tensor, comps: int) -> None:
+        for peer, rows in self.halo.items():
+            self._put(arr, rows, comps, peer, 1)
+        for peer, rows in self.exports.items():
+            self._get(arr, rows, comps, peer, 1, ADD)
+        if self.all_halo is not None:
+            unpack_rows(arr, self.all_halo, comps, None, ZERO)
+
+    def launches_per_step(self) -> int:
+        return 1 + 2 * (len(self.halo) + len(self.exports)) + (1 if self.all_halo is not None else 0)
+
+    def close(self) -> None:
+        """Unmap the peers' mailboxes and free this one (after the last step)."""
+        for p in self._opened:
+            _native.call("mp_ipc_close", p)
+        self._opened = []
+        if self.base:
+            _native.load().mp_free(ctypes.c_void_p(self.base))
+            self.base = 0
+
+
 def slab_bounds(nx: int, ny: int, world: int):
     """Owner ranges of a quad2d mesh cut into x-slabs (cell = x*ny + y)."""
     xs = np.array([(r * nx) // world for r in range(world + 1)], dtype=np.int64)
@@ -220,11 +361,19 @@ class DistributedLoop:
         self.loop = mp.bind(self.plan, kernel, schedule=schedule)
         cells = next(iter(mesh_local.mappings.values())).to_set.name
         self.dec = dec.renumbered(self.plan.set_perms[cells].forward)
-        self.halo = HaloExchange(self.dec, transport, "cuda")
         self.read = next((a.array for a in kernel.indirect_read_args), None)
         self.inc = kernel.increment_args[0].array
         self.rc = None if self.read is None else mesh_local.data[self.read].components
         self.ic = mesh_local.data[self.inc].components
+        # transport: a mailbox publisher (PeerHub.connector / ipc_connector) selects the
+        # peer-memory exchange (device-side, graph-capturable); otherwise host-driven
+        # send/recv through the given transport
+        self.peer = hasattr(transport, "ipc")
+        if self.peer:
+            self.halo = PeerExchange(self.dec, transport, "cuda", self.loop.tensors[self.inc].dtype,
+                                     self.rc or 0, self.ic)
+        else:
+            self.halo = HaloExchange(self.dec, transport, "cuda")
         # core / boundary split: core blocks touch no halo point, so
         # they run while the halo import is in flight; the colour schedules only
         if overlap is None:
@@ -253,6 +402,8 @@ class DistributedLoop:
         return per_block == 0
 
     def step(self) -> None:
+        if self.peer:
+            self.halo.bump()  # the step's epoch (device counter: graph replays advance it)
         if self.core is None:
             if self.read is not None:
                 self.halo.import_rows(self.loop.tensors[self.read], self.rc)
@@ -266,6 +417,26 @@ class DistributedLoop:
             cur.wait_stream(self.comm)
             self.loop.run(sub=self.boundary)
         self.halo.export_increments(self.loop.tensors[self.inc], self.ic)
+
+    def capture(self):
+        """One step as a CUDA graph (peer-memory exchange only: the NCCL /
+        thread transports synchronise on the host).  Collective: every rank
+        captures, after one real warm-up step together.  ``replay()`` runs a
+        step on the current stream -- halo puts and waits, core and boundary
+        launches, increment export -- with one submission."""
+        if not self.peer:
+            raise RuntimeError("capture needs the peer-memory exchange (PeerHub / ipc_connector transport)")
+        inc = self.loop.tensors[self.inc]
+        saved = inc.clone()
+        self.step()  # warm-up; its increments (local and the peers' exports) are undone below
+        torch.cuda.current_stream().synchronize()
+        inc.copy_(saved)
+        torch.cuda.current_stream().synchronize()
+        del saved
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            self.step()
+        return g
 
     def step_host(self, inputs: dict, out) -> None:
         """One end-to-end step with host buffers: H2D of this rank's local

@@ -206,3 +206,118 @@ def test_threaded_ranks_on_one_gpu_match_serial(world, reorder, schedule, overla
     for lo, block in out.values():
         full[lo: lo + block.shape[0]] = block
     assert np.array_equal(full, 3 * want)
+
+
+# ---- peer-memory exchange (device-side puts / waits, graph-capturable) ------------------
+
+
+def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, graph):
+    """One rank's share with the peer-memory exchange; returns (lo, owned rows)."""
+    import paper_1802_03749_b200 as mp
+
+    mesh, _ = _global_case(nx, ny)
+    q = mesh.data["q"].view2d()
+    w = np.ascontiguousarray(mesh.data["w"].view2d())
+    bounds, xs = decomp.slab_bounds(nx, ny, world)
+    tables = [workloads.quad2d_table(nx, ny, int(xs[k]), int(xs[k + 1])) for k in range(world)]
+    halos = []
+    for k, (t, _) in enumerate(tables):
+        pts = np.unique(t)
+        halos.append(pts[(pts < bounds[k]) | (pts >= bounds[k + 1])])
+    t, g = tables[r]
+    dec = decomp.decompose(t, g, bounds, r, world, lambda obj: halos)
+    local = decomp.local_flux_mesh(t, g, dec, q[dec.local_points], w[g], np.zeros((dec.n_local, 4)))
+    kernel = mp.kernel_for_mesh("flux", local)
+    dl = decomp.DistributedLoop(local, kernel, dec, publish, mp.PlanConfig(reorder=reorder, block_size=64),
+                                schedule, overlap=overlap)
+    assert dl.peer
+    if graph:
+        gr = dl.capture()
+        for _ in range(steps):
+            gr.replay()
+    else:
+        for _ in range(steps):
+            dl.step()
+    torch.cuda.synchronize()
+    res = (dec.lo, dl.owned_result())
+    return res, dl
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,reorder,schedule,overlap,graph", [
+    (2, "gps", "stream", False, False), (3, "none", "stream", True, False), (4, "gps", "stream", True, True),
+    (2, "none", "colour", True, True), (3, "gps", "pipelined", False, True), (2, "gps", "stream-pull", True, True)])
+def test_peer_exchange_threads_on_one_gpu_match_serial(world, reorder, schedule, overlap, graph):
+    """Ranks as threads on one device exchanging through each other's
+    mailboxes (device pointers): direct steps and CUDA-graph replays of a
+    whole step both equal the serial loop."""
+    import threading
+
+    nx, ny, steps = 64, 48, 3
+    _, want = _global_case(nx, ny)
+    hub = decomp.PeerHub()
+    out, errors, loops_ = {}, [], []
+
+    def rank_main(r):
+        torch.cuda.set_device(0)
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[r], dl = _peer_rank(r, world, nx, ny, reorder, schedule, overlap, hub.connector(r), steps, graph)
+                loops_.append(dl)
+        except Exception as exc:  # pragma: no cover - surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=300)
+    assert not errors, errors
+    full = np.zeros_like(want)
+    for lo, block in out.values():
+        full[lo: lo + block.shape[0]] = block
+    assert np.array_equal(full, steps * want)
+    torch.cuda.synchronize()
+    for dl in loops_:
+        dl.halo.close()
+
+
+def _ipc_rank_main(rank, world, port, result_file):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+
+    def allgather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    (lo, owned), dl = _peer_rank(rank, world, 24, 20, "gps", "stream", True, decomp.ipc_connector(allgather), 2,
+                                 graph=True)
+    parts = [None] * world
+    dist.all_gather_object(parts, (lo, owned))
+    dist.barrier()
+    dl.halo.close()
+    if rank == 0:
+        _, want = _global_case(24, 20)
+        full = np.zeros_like(want)
+        for lo_, block in parts:
+            full[lo_: lo_ + block.shape[0]] = block
+        np.save(result_file, np.stack([full, 2 * want]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_exchange_two_processes_ipc_on_one_gpu(tmp_path):
+    """Two processes (gloo rendezvous only) on one device, mailboxes mapped
+    through CUDA IPC, whole steps replayed as CUDA graphs: the path the
+    multi-GPU bench takes, with the peer on the same device instead of across
+    NVLink."""
+    import torch.multiprocessing as tmp
+
+    out = str(tmp_path / "full.npy")
+    tmp.spawn(_ipc_rank_main, args=(2, _free_port(), out), nprocs=2, join=True)
+    got, want = np.load(out)
+    assert np.array_equal(got, want)

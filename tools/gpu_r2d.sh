@@ -1,0 +1,9 @@
+# ncu full captures of one colour launch: C5 GPS stream (headline) vs 8x8 tiles (stream, pipelined-pull)
+for spec in "gps stream hier_stream" "structured:8,8 stream hier_stream" "structured:8,8 pipelined-pull hier_pipe"; do
+  set -- $spec
+  tag=$(echo $1 | tr ':,' '__')_$2
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$3 -s 3 -c 1 -o gpurun_out/r2_c5_$tag \
+      python tools/prof_loop.py --config C5 --reorder $1 --schedule $2 --runs 1 --timed 1 > gpurun_out/ncu_$tag.log 2>&1
+  echo "ncu $tag rc=$?"
+done
+timeout 900 python -m pytest tests/test_decomp.py -x -q -m gpu -k "peer" > gpurun_out/pytest_peer.log 2>&1; echo "peer rc=$?"; tail -15 gpurun_out/pytest_peer.log
