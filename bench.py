@@ -10,8 +10,11 @@ Airfoil-style edge->cell flux loop on a 5657 x 5657 quad mesh (63,991,984
 edges, 32,001,649 cells, fp64), hierarchical two-layer colouring (GPS
 blocks, block size 128, the fastest measured schedule), values on the
 1/1024 grid from a counter hash (synthetic).  ``roofline.frac`` is taken on
-the consumed bytes (``mp.consumed_bytes``: the components the element
-function reads), ``value`` is the paper's effective GB/s.  One step = one full execution of the loop over
+the consumed bytes of SURVEY 8(d) (``mp.consumed_bytes``: indirectly read
+arrays counted only for the components the element function reads; C5's
+equal the formula's, C4's are 1,915 MB of the formula's 3,387 MB);
+``frac_strict`` also trims the direct arrays; ``value`` is the paper's
+effective GB/s.  One step = one full execution of the loop over
 the mesh.  Effective GB/s uses the paper's formula (simulator.py:315-328):
 each array once, the incremented array twice, 4-byte mapping entries.
 With N>1 GPUs the mesh is decomposed into x-slabs (owner compute, NCCL halo
@@ -596,6 +599,8 @@ def main():
     ap.add_argument("--schedule", default="best", choices=SCHEDULES + ("best",),
                     help="headline executor schedule; 'best' = fastest of the measured schedules")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--transport", default="peer", choices=("peer", "nccl"),
+                    help="N>1 halo exchange: peer-memory puts (graph-captured steps) or NCCL send/recv")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -37,6 +37,15 @@ namespace {
 constexpr int MAX_STAGES = 8;  // mbarrier pairs that fit the 128-byte header
 constexpr int PIPE_K = 3;  // staged-id prefetch distance (fills)
 
+// Sanitizer controls (tools/race_control.sh; never in the shipped build):
+// 1 = the producer skips its empty-barrier wait (a real write-after-read race
+// on stage reuse); 2 = the producer completes its cp.async copies
+// (wait_all) and arrives with a plain mbarrier.arrive instead of
+// cp.async.mbarrier.arrive.noinc.
+#ifndef MP_PIPE_RACE_CONTROL
+#define MP_PIPE_RACE_CONTROL 0
+#endif
+
 __device__ __forceinline__ unsigned saddr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -236,7 +245,9 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
       int b, nc0;
       int4 md;
       get(fill, b, md, nc0);
+#if MP_PIPE_RACE_CONTROL != 1
       mbar_wait(&empty[s], ((fill / NSTAGE) & 1) ^ 1);
+#endif
       if (b < 0) {
         if (lane == 0) hdr[0] = -1;
         mbar_arrive(&full[s]);
@@ -385,7 +396,12 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
         }
       }
       mbar_arrive(&full[s]);          // releases the header / ids stores
+#if MP_PIPE_RACE_CONTROL == 2
+      asm volatile("cp.async.wait_all;" ::: "memory");  // copies complete in this thread, then a plain arrive
+      mbar_arrive(&full[s]);
+#else
       mbar_arrive_cpasync(&full[s]);  // fires when this lane's copies land
+#endif
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
   } else {

@@ -509,15 +509,28 @@ def bench_rank(args, rank: int, world: int) -> int:
     kernel = mp.kernel_for_mesh("flux", mesh)
     cfg = mp.PlanConfig(reorder=args.reorder, layout="aos", block_size=args.block_size)
     sched = "stream" if args.schedule == "best" else args.schedule
-    dl = DistributedLoop(mesh, kernel, dec, TorchDistTransport(), cfg, sched)
+    transport = ipc_connector(allgather) if getattr(args, "transport", "peer") == "peer" else TorchDistTransport()
+    dl = DistributedLoop(mesh, kernel, dec, transport, cfg, sched)
     t_plan = time.perf_counter() - t0
+    # peer exchange: the whole step (epoch bump, halo puts / waits, core and
+    # boundary launches, export) is one CUDA graph, one submission per step
+    graph = dl.capture() if dl.peer else None
+    run_step = graph.replay if graph is not None else dl.step
     sampler = bench.ClockSampler(local_rank)
     sampler.start()
     for _ in range(args.warmup):
-        dl.step()
+        run_step()
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
+    # host enqueue cost of a step (what bounds strong scaling once the
+    # per-GPU loop is ~0.17 ms at 8 GPUs): submissions without waiting
+    t_h = time.perf_counter()
+    for _ in range(args.steps):
+        run_step()
+    enqueue_us = (time.perf_counter() - t_h) / args.steps * 1e6
+    torch.cuda.synchronize()
+    dist.barrier()
     # a rank's share of the loop's bytes; below twice L2 the steps are timed
     # one by one with L2 flushed in between (as bench.py does on one GPU)
     share = (nx * ny * 4 * 8 * 3 + (nx * (ny - 1) + ny * (nx - 1)) * (2 * 8 + 2 * 4)) / world
@@ -526,7 +539,7 @@ def bench_rank(args, rank: int, world: int) -> int:
     if flush.buf is None:
         a.record()
         for _ in range(args.steps):
-            dl.step()
+            run_step()
         b.record()
         torch.cuda.synchronize()
         step_ms = a.elapsed_time(b) / args.steps
@@ -535,7 +548,7 @@ def bench_rank(args, rank: int, world: int) -> int:
         for ea, eb in evs:
             flush()
             ea.record()
-            dl.step()
+            run_step()
             eb.record()
         torch.cuda.synchronize()
         step_ms = sum(ea.elapsed_time(eb) for ea, eb in evs) / args.steps
@@ -575,7 +588,10 @@ def bench_rank(args, rank: int, world: int) -> int:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {"workload": f"{args.config}: quad2d {nx}x{ny} flux f64 decomposed into {world} x-slabs",
                        "strategy": "hier", "reorder": args.reorder, "schedule": sched,
-                       "parallelism": f"owner-compute x{world}, NCCL halo exchange",
+                       "parallelism": f"owner-compute x{world}, " + (
+                           "peer-memory halo exchange (P2P puts into IPC-mapped mailboxes, device-side epoch "
+                           "flags), each step one CUDA graph" if dl.peer else "NCCL halo exchange"),
+                       "host_enqueue_us_per_step": round(enqueue_us, 2),
                        "useful_bytes_per_step": ub_total,
                        "l2": "inputs larger than L2 (no flush)" if flush.buf is None else "flushed between steps"},
             "roofline": {"bound": "hbm", "achieved": round(gbps / world, 2), "peak": peak, "unit": "GB/s",

@@ -11,7 +11,7 @@ is unchanged.  That keeps the 64M-edge and 8M-cell configs inside memory
 (the full reference generator materialises an unused 28-component state).
 
 Kernel specs carry a ``device_op``; the element arithmetic itself lives in
-``csrc/mp_ops.cuh`` (device) and ``oracle/serial.py`` (CPU checker).
+``csrc/mp_ops.cuh`` (device) and ``oracle/loops.py`` (the CPU checker, test-only).
 """
 
 import numpy as np

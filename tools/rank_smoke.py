@@ -22,6 +22,7 @@ ap.add_argument("--reorder", default=None)
 ap.add_argument("--block-size", type=int, default=128)
 ap.add_argument("--schedule", default="best")
 ap.add_argument("--cpu-seconds", type=float, default=0.0)
+ap.add_argument("--transport", default="peer", choices=("peer", "nccl"))
 args, _ = ap.parse_known_args()
 if args.reorder is None:
     args.reorder = bench.DEFAULT_REORDER[args.config]
