@@ -244,6 +244,16 @@ mp_status mp_plan_thread_colours(int32_t nb, const int32_t* block_offsets, const
                                  int32_t arity, int32_t map_layout, uint32_t written_mask, int32_t max_block,
                                  int32_t* colours, int32_t* counts, int32_t* sorted_order, void* stream);
 
+/* Executor layout of each block's staged rows (not part of the plan):
+ * perm[staged_offsets[b] + position] = staged index placed at that shared
+ * row, chosen so that each quarter-warp access group (colour-loop
+ * read-modify-writes, element reads; thread_colours colour-sorted per block)
+ * touches rows in distinct classes mod 8, i.e. distinct 16-byte bank groups.
+ * local_slots: per (element, slot) staged index, 0xFFFF when not staged. */
+mp_status mp_plan_row_placement(int32_t nb, const int32_t* block_offsets, const int32_t* staged_offsets,
+                                const uint16_t* local_slots, int32_t arity, const uint8_t* thread_colours,
+                                int32_t* perm, void* stream);
+
 /* Greedy colouring of the plan blocks over their written points, on the
  * device (replaces _accel.greedy_colour_csr at plan.py:254 in
  * _colour_blocks_ns, plan.py:241-257): bit-identical to greedy_colour_csr

@@ -178,7 +178,14 @@ extern "C" mp_status mp_mailbox_alloc(int64_t bytes, void** ptr) {
   mp::clear_error();
   *ptr = nullptr;
   MP_CUDA_TRY(cudaMalloc(ptr, bytes > 0 ? (size_t)bytes : 256));
-  MP_CUDA_TRY(cudaMemset(*ptr, 0, bytes > 0 ? (size_t)bytes : 256));
+  // zeroed before the caller publishes it: a peer's first put may follow at
+  // once, on a stream that does not order after the legacy default stream
+  cudaStream_t s;
+  MP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemsetAsync(*ptr, 0, bytes > 0 ? (size_t)bytes : 256, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  MP_CUDA_TRY(e);
   return MP_OK;
 }
 

@@ -238,6 +238,84 @@ size_t thread_colour_smem(int max_block, int nsl) {
   return (size_t)mmax * 8 + (size_t)max_block * W * 4 + (size_t)max_block * 12 + (size_t)W * 4 + 16;
 }
 
+
+// ---- shared-memory row placement (executor layout; the plan is unchanged) -----------
+// The executors keep staged row j of a block at shared row j, 32-byte rows
+// swizzled so that any 8 rows with distinct j mod 8 fall in 8 distinct 16-byte
+// bank groups (exec_hier_stream.cu RowFmt).  A quarter-warp (8 lanes) access
+// of 16-byte granules is conflict-free exactly when its rows are distinct mod
+// 8.  Blocks whose elements touch staged rows in strided patterns (compact
+// tiles: an edge colour class visits every other cell) conflict 2-4 ways.
+// This pass renumbers each block's staged rows so that the rows of each
+// quarter-warp access group land in distinct classes mod 8: groups are the
+// colour-loop read-modify-writes (lanes t..t+7 of one thread colour, one
+// slot) and then the element reads (lanes t..t+7, one slot); a greedy
+// assigns each unplaced row the class with the most room not yet used in its
+// group.  Class c holds positions c, c+8, ... (ns/8 rounded per class), so the
+// renumbering is a permutation of 0..ns-1; perm[s0 + position] = old row.
+constexpr int RP_MAXS = 4096;
+
+__global__ void row_placement_kernel(int32_t nb, const int32_t* __restrict__ bo, const int32_t* __restrict__ st_off,
+                                     const uint16_t* __restrict__ ls, int arity, const uint8_t* __restrict__ tcol,
+                                     int32_t* perm) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const int e0 = bo[b], k = bo[b + 1] - e0, s0 = st_off[b], ns = st_off[b + 1] - s0;
+  if (ns > RP_MAXS) {  // identity (the host checks the maximum first)
+    for (int r = 0; r < ns; ++r) perm[s0 + r] = r;
+    return;
+  }
+  int8_t cls[RP_MAXS];
+  for (int r = 0; r < ns; ++r) cls[r] = -1;
+  int cap[8];
+  for (int c = 0; c < 8; ++c) cap[c] = ns / 8 + (c < ns % 8 ? 1 : 0);
+  auto place = [&](const int* rows, int n) {
+    unsigned used = 0;
+    for (int i = 0; i < n; ++i)
+      if (cls[rows[i]] >= 0) used |= 1u << cls[rows[i]];
+    for (int i = 0; i < n; ++i) {
+      const int r = rows[i];
+      if (cls[r] >= 0) continue;
+      int best = -1;
+      for (int pass = 0; pass < 2 && best < 0; ++pass)
+        for (int c = 0; c < 8; ++c)
+          if (cap[c] > 0 && (pass == 1 || !(used >> c & 1u)) && (best < 0 || cap[c] > cap[best])) best = c;
+      cls[r] = (int8_t)best;
+      --cap[best];
+      used |= 1u << best;
+    }
+  };
+  int rows[8];
+  for (int pass = 0; pass < 2; ++pass)  // 0: colour-loop groups, 1: element reads
+    for (int q = 0; q < arity; ++q)
+      for (int t0 = 0; t0 < k; t0 += 8) {
+        const int t1 = t0 + 8 < k ? t0 + 8 : k;
+        int t = t0;
+        while (t < t1) {  // runs of one thread colour (colour-sorted elements)
+          const int c = tcol[e0 + t];
+          int n = 0;
+          for (; t < t1 && (pass == 1 || tcol[e0 + t] == c); ++t) {
+            const int r = ls[(int64_t)(e0 + t) * arity + q];
+            if (r == 0xFFFF || r >= ns) continue;
+            bool dup = false;
+            for (int i = 0; i < n; ++i) dup |= rows[i] == r;
+            if (!dup) rows[n++] = r;
+          }
+          place(rows, n);
+        }
+      }
+  int idx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r = 0; r < ns; ++r) {
+    int c = cls[r];
+    if (c < 0) {  // a staged row no element touches through a staged slot
+      c = 0;
+      for (int d = 1; d < 8; ++d)
+        if (cap[d] > cap[c]) c = d;
+      --cap[c];
+    }
+    perm[s0 + c + 8 * idx[c]++] = r;
+  }
+}
 }  // namespace
 }  // namespace mp
 
@@ -306,5 +384,16 @@ extern "C" mp_status mp_plan_thread_colours(int32_t nb, const int32_t* block_off
   MP_CUDA_TRY(cudaFreeAsync(d_over, st));
   MP_CUDA_TRY(cudaStreamSynchronize(st));
   if (over != INT_MAX) MP_FAIL(MP_ERR_CAPACITY, "block %d needs more than 256 thread colours", over);
+  return MP_OK;
+}
+
+extern "C" mp_status mp_plan_row_placement(int32_t nb, const int32_t* block_offsets, const int32_t* staged_offsets,
+                                          const uint16_t* local_slots, int32_t arity, const uint8_t* thread_colours,
+                                          int32_t* perm, void* stream) {
+  clear_error();
+  if (nb == 0) return MP_OK;
+  mp::row_placement_kernel<<<(nb + 127) / 128, 128, 0, as_stream(stream)>>>(nb, block_offsets, staged_offsets,
+                                                                            local_slots, arity, thread_colours, perm);
+  MP_CHECK_LAUNCH();
   return MP_OK;
 }

@@ -550,6 +550,42 @@ def pull_lists(bo: torch.Tensor, ls16: torch.Tensor, arity: int, st_off: torch.T
     return off, ref16
 
 
+#: executor layout of the staged rows: bank-group placement (mp_plan_row_placement)
+ROW_PLACEMENT = os.environ.get("MESHPLAN_ROW_PLACEMENT", "0") == "1"
+
+
+def place_rows(bo, st_off, st_ids, ls, arity: int, tcol_sorted):
+    """Renumber each block's staged rows for conflict-free quarter-warp
+    shared-memory access (``mp_plan_row_placement``): the staged id lists are
+    permuted within their blocks and the local slots remapped, consistently
+    for every executor structure derived from them.  The plan itself (its
+    ascending staged lists, HierarchicalPlan.staged) is unchanged; results are
+    bit-identical (a slot is a storage position, not an order)."""
+    dev = bo.device
+    total = st_ids.numel()
+    perm = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    tc = tcol_sorted.to(torch.uint8).contiguous()
+    _native.call("mp_plan_row_placement", bo.numel() - 1, _native.ptr(bo), _native.ptr(st_off), _native.ptr(ls),
+                 int(arity), _native.ptr(tc), _native.ptr(perm), _sp())
+    counts = (st_off[1:] - st_off[:-1]).long()
+    base = torch.repeat_interleave(st_off[:-1].long(), counts)
+    old = base + perm[:total].long()
+    new_ids = st_ids[old]
+    inv = torch.empty(total, dtype=torch.long, device=dev)
+    inv[old] = torch.arange(total, device=dev) - base  # flattened (block, old local) -> new local
+    # remap per (element, slot): old local index -> new local index within the element's block
+    n_el = int(bo[-1])
+    sizes = (bo[1:] - bo[:-1]).long()
+    blk_of_ref = torch.repeat_interleave(torch.arange(bo.numel() - 1, device=dev), sizes * arity)
+    lsl = ls[: n_el * arity].long() & 0xFFFF
+    staged = lsl != 0xFFFF
+    idx = st_off[:-1].long()[blk_of_ref] + torch.where(staged, lsl, torch.zeros_like(lsl))
+    new_ls = torch.where(staged, inv[idx], lsl)
+    out = ls.clone()
+    out[: n_el * arity] = new_ls.to(torch.int16)
+    return new_ids.to(torch.int32), out
+
+
 def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sorted_d, tcounts_d, st_off, st_ids,
                       wr_off, wr_ids, stage_mask, stage_reads, npts, block_size) -> DevicePlan:
     """Assemble the executor structures (slots, schedules) from plan arrays."""
@@ -558,6 +594,10 @@ def build_device_hier(map_d, block_offsets_np, block_colours_np, ncol, tcol_sort
     nb = bo.numel() - 1
     ls, ws = local_slots(bo, map_d, stage_mask, st_off, st_ids, wr_off, wr_ids)
     counts = (st_off[1:] - st_off[:-1]) if nb else torch.zeros(0, dtype=torch.int32, device=dev)
+    if ROW_PLACEMENT and nb and torch.equal(st_off, wr_off) and torch.equal(st_ids, wr_ids) and \
+            int(counts.max()) <= 4096:
+        st_ids, ls = place_rows(bo, st_off, st_ids, ls, map_d.shape[1], tcol_sorted_d)
+        wr_ids = st_ids
     max_staged = int(counts.max()) if nb else 0
     arity = map_d.shape[1]
     full_mask = stage_mask == (1 << arity) - 1

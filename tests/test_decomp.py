@@ -211,8 +211,11 @@ def test_threaded_ranks_on_one_gpu_match_serial(world, reorder, schedule, overla
 # ---- peer-memory exchange (device-side puts / waits, graph-capturable) ------------------
 
 
-def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, graph):
-    """One rank's share with the peer-memory exchange; returns (lo, owned rows)."""
+def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, graph, barrier=lambda: None):
+    """One rank's share with the peer-memory exchange; returns (lo, owned rows).
+    ``barrier`` separates setup from stepping: ranks sharing one device must
+    not synchronise the whole device (plan building does) while a peer's
+    exchange kernel waits for them."""
     import paper_1802_03749_b200 as mp
 
     mesh, _ = _global_case(nx, ny)
@@ -231,14 +234,17 @@ def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, gra
     dl = decomp.DistributedLoop(local, kernel, dec, publish, mp.PlanConfig(reorder=reorder, block_size=64),
                                 schedule, overlap=overlap)
     assert dl.peer
+    barrier()
     if graph:
         gr = dl.capture()
+        barrier()
         for _ in range(steps):
             gr.replay()
     else:
         for _ in range(steps):
             dl.step()
-    torch.cuda.synchronize()
+    torch.cuda.current_stream().synchronize()
+    barrier()
     res = (dec.lo, dl.owned_result())
     return res, dl
 
@@ -257,15 +263,18 @@ def test_peer_exchange_threads_on_one_gpu_match_serial(world, reorder, schedule,
     _, want = _global_case(nx, ny)
     hub = decomp.PeerHub()
     out, errors, loops_ = {}, [], []
+    bar = threading.Barrier(world, timeout=240)
 
     def rank_main(r):
         torch.cuda.set_device(0)
         try:
             with torch.cuda.stream(torch.cuda.Stream()):
-                out[r], dl = _peer_rank(r, world, nx, ny, reorder, schedule, overlap, hub.connector(r), steps, graph)
+                out[r], dl = _peer_rank(r, world, nx, ny, reorder, schedule, overlap, hub.connector(r), steps, graph,
+                                        bar.wait)
                 loops_.append(dl)
         except Exception as exc:  # pragma: no cover - surfaced below
             errors.append(exc)
+            bar.abort()
 
     threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
     for th in threads:
@@ -295,7 +304,7 @@ def _ipc_rank_main(rank, world, port, result_file):
         return out
 
     (lo, owned), dl = _peer_rank(rank, world, 24, 20, "gps", "stream", True, decomp.ipc_connector(allgather), 2,
-                                 graph=True)
+                                 graph=True, barrier=dist.barrier)
     parts = [None] * world
     dist.all_gather_object(parts, (lo, owned))
     dist.barrier()
