@@ -69,6 +69,9 @@
 
 #include "mp_loop.cuh"
 
+#ifndef MP_ROW256
+#define MP_ROW256 1  // 256-bit global accesses for 32-byte increment rows
+#endif
 #ifndef MP_STREAM_MAXREG
 #define MP_STREAM_MAXREG 72  // 7 CTAs of 128 threads per SM
 #endif
@@ -247,7 +250,18 @@ __device__ __forceinline__ void gather_row(unsigned char* base, int r, const T* 
 template <typename T, int NC, int LAYOUT>
 __device__ __forceinline__ void ldg_row(const T* g, int64_t p, int64_t npts, bool cg, T (&out)[NC]) {
   constexpr int RB = NC * (int)sizeof(T);
-  if constexpr (LAYOUT == MP_AOS) {
+  if constexpr (LAYOUT == MP_AOS && RB == 32 && MP_ROW256) {
+    // one 256-bit access per 32-byte row (LDG.E.ENL2.256): one LSU request
+    // per lane instead of two 16-byte ones
+    const T* src = g + p * NC;
+    unsigned long long a, b, c, d;
+    if (cg)
+      asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(src));
+    else
+      asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(src));
+    const unsigned long long w[4] = {a, b, c, d};
+    memcpy(out, w, 32);
+  } else if constexpr (LAYOUT == MP_AOS) {
     constexpr int G = RB % 16 == 0 ? 16 : (RB % 8 == 0 ? 8 : 4);
     using V = typename Gran<G>::type;
     const V* src = reinterpret_cast<const V*>(g + p * NC);
@@ -271,7 +285,13 @@ constexpr int CTL_BYTES = CTL_RING * 4 + MAX_NS * 8;
 // registers -> global row (point p) of the incremented array
 template <typename T, int NC, int LAYOUT>
 __device__ __forceinline__ void stg_row(T* g, int64_t p, int64_t npts, const T (&in)[NC]) {
-  if constexpr (LAYOUT == MP_AOS) {
+  if constexpr (LAYOUT == MP_AOS && NC * (int)sizeof(T) == 32 && MP_ROW256) {
+    unsigned long long w[4];
+    memcpy(w, in, 32);
+    asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(g + p * NC), "l"(w[0]), "l"(w[1]), "l"(w[2]),
+                 "l"(w[3])
+                 : "memory");
+  } else if constexpr (LAYOUT == MP_AOS) {
     constexpr int RB = NC * (int)sizeof(T);
     constexpr int GG = RB % 16 == 0 ? 16 : (RB % 8 == 0 ? 8 : 4);
     using V = typename Gran<GG>::type;
@@ -669,21 +689,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
         if (DATAFLOW && rows_late) ldg_row<T, IC, LAYOUT>(v.inc, p, v.npts, true, rrow[r]);
 #pragma unroll
         for (int c = 0; c < IC; ++c) acc[c] = rrow[r][c] + acc[c];
-        if constexpr (LAYOUT == MP_AOS) {
-          constexpr int RB = IC * (int)sizeof(T);
-          constexpr int GG = RB % 16 == 0 ? 16 : (RB % 8 == 0 ? 8 : 4);
-          using V = typename Gran<GG>::type;
-          unsigned char* dst = reinterpret_cast<unsigned char*>(v.inc + p * IC);
-#pragma unroll
-          for (int ch = 0; ch < RB / GG; ++ch) {
-            V x;
-            memcpy(&x, reinterpret_cast<const unsigned char*>(acc) + ch * GG, GG);
-            *reinterpret_cast<V*>(dst + ch * GG) = x;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < IC; ++c) v.inc[(int64_t)c * v.npts + p] = acc[c];
-        }
+        stg_row<T, IC, LAYOUT>(v.inc, p, v.npts, acc);
       }
     }
     }  // push form

@@ -418,21 +418,29 @@ class DistributedLoop:
             self.loop.run(sub=self.boundary)
         self.halo.export_increments(self.loop.tensors[self.inc], self.ic)
 
-    def capture(self):
-        """One step as a CUDA graph (peer-memory exchange only: the NCCL /
-        thread transports synchronise on the host).  Collective: every rank
-        captures, after one real warm-up step together.  ``replay()`` runs a
-        step on the current stream -- halo puts and waits, core and boundary
-        launches, increment export -- with one submission."""
-        if not self.peer:
-            raise RuntimeError("capture needs the peer-memory exchange (PeerHub / ipc_connector transport)")
+    def warmup_step(self) -> None:
+        """One real step (collective) whose effect on the increment array --
+        local increments and the peers' exports -- is undone afterwards:
+        primes kernel attributes and allocations before a capture."""
         inc = self.loop.tensors[self.inc]
         saved = inc.clone()
-        self.step()  # warm-up; its increments (local and the peers' exports) are undone below
+        self.step()
         torch.cuda.current_stream().synchronize()
         inc.copy_(saved)
         torch.cuda.current_stream().synchronize()
-        del saved
+
+    def capture(self, warmup: bool = True):
+        """One step as a CUDA graph (peer-memory exchange only: the NCCL /
+        thread transports synchronise on the host).  Collective when
+        ``warmup`` (every rank runs ``warmup_step`` together first).
+        ``replay()`` runs a step on the current stream -- halo puts and
+        waits, core and boundary launches, increment export -- with one
+        submission.  Ranks that are threads of one process must capture one
+        at a time (capture synchronises the device)."""
+        if not self.peer:
+            raise RuntimeError("capture needs the peer-memory exchange (PeerHub / ipc_connector transport)")
+        if warmup:
+            self.warmup_step()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
             self.step()

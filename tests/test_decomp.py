@@ -211,7 +211,8 @@ def test_threaded_ranks_on_one_gpu_match_serial(world, reorder, schedule, overla
 # ---- peer-memory exchange (device-side puts / waits, graph-capturable) ------------------
 
 
-def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, graph, barrier=lambda: None):
+def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, graph, barrier=lambda: None,
+               capture_lock=None):
     """One rank's share with the peer-memory exchange; returns (lo, owned rows).
     ``barrier`` separates setup from stepping: ranks sharing one device must
     not synchronise the whole device (plan building does) while a peer's
@@ -236,7 +237,13 @@ def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, gra
     assert dl.peer
     barrier()
     if graph:
-        gr = dl.capture()
+        dl.warmup_step()
+        barrier()
+        if capture_lock is not None:  # threads of one process capture one at a time
+            with capture_lock:
+                gr = dl.capture(warmup=False)
+        else:
+            gr = dl.capture(warmup=False)
         barrier()
         for _ in range(steps):
             gr.replay()
@@ -264,13 +271,14 @@ def test_peer_exchange_threads_on_one_gpu_match_serial(world, reorder, schedule,
     hub = decomp.PeerHub()
     out, errors, loops_ = {}, [], []
     bar = threading.Barrier(world, timeout=240)
+    cap_lock = threading.Lock()
 
     def rank_main(r):
         torch.cuda.set_device(0)
         try:
             with torch.cuda.stream(torch.cuda.Stream()):
                 out[r], dl = _peer_rank(r, world, nx, ny, reorder, schedule, overlap, hub.connector(r), steps, graph,
-                                        bar.wait)
+                                        bar.wait, cap_lock)
                 loops_.append(dl)
         except Exception as exc:  # pragma: no cover - surfaced below
             errors.append(exc)
