@@ -42,6 +42,10 @@ sys.path.insert(0, str(REPO))
 #: SURVEY 8d), the reference's k-way partition for the face loop (the config
 #: names k-way partitioned blocks; ~50 s to plan at 24M faces)
 DEFAULT_REORDER = {"C1": "gps", "C2": "gps", "C3": "none", "C4": "partition", "C5": "gps"}
+#: default block size per config (--block-size overrides): the k-way blocks of
+#: the face loop at 256 faces (reuse 3.22 vs 2.92 at 128; pipelined-pull
+#: 1.02 vs 1.08 ms, tools/gpu_c4bs.sh), 128 elsewhere
+DEFAULT_BLOCK = {"C4": 256}
 #: other block layouts timed beside the headline (reported as vs_layout):
 #: name -> (reorder, block size or None for --block-size, schedule(s) or None for the headline's)
 COMPARE_REORDER = {"C2": (("none", None, None),),
@@ -595,7 +599,7 @@ def main():
     ap.add_argument("--reorder", default=None, help="block layout (default: per config, DEFAULT_REORDER)")
     ap.add_argument("--global-reorder", default="gps")
     ap.add_argument("--layout", default="aos")
-    ap.add_argument("--block-size", type=int, default=128)
+    ap.add_argument("--block-size", type=int, default=None)
     ap.add_argument("--schedule", default="best", choices=SCHEDULES + ("best",),
                     help="headline executor schedule; 'best' = fastest of the measured schedules")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -606,6 +610,8 @@ def main():
         args.warmup = 3
     if args.reorder is None:
         args.reorder = DEFAULT_REORDER[args.config]
+    if args.block_size is None:
+        args.block_size = DEFAULT_BLOCK.get(args.config, 128)
     if args.impl == "reference":
         return reference_arm(args)
     return our_arm(args)

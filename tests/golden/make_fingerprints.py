@@ -51,6 +51,9 @@ CONFIGS = {
     "C4s": ("hex3d-faces", (60, 60, 60), "face-flux", "f64", "increment-only",
             [("hier", "none"), ("hier", "partition")], [("hier", "partition")]),
     "C4": ("hex3d-faces", (200, 200, 200), "face-flux", "f64", "increment-only", [("hier", "partition")], []),
+    # the bench's C4 headline plan: the same k-way partition at block size 256
+    "C4k256": ("hex3d-faces", (200, 200, 200), "face-flux", "f64", "increment-only", [("hier", "partition")], [],
+               256),
     "C5": ("quad2d", (5657, 5657), "flux", "f64", "all-indirect", [("hier", "gps"), ("global", "gps")], []),
 }
 INC = {"flux": "res", "flux-noread": "res", "scatter8": "force", "face-flux": "flux", "face-flux-heavy": "flux"}
@@ -100,14 +103,15 @@ def plan_record(plan, m):
 def main(names):
     out = json.loads(OUT.read_text()) if OUT.exists() else {}
     for name in names:
-        family, dims, kname, dtype, staging, strategies, rand_runs = CONFIGS[name]
+        family, dims, kname, dtype, staging, strategies, rand_runs = CONFIGS[name][:7]
+        bs = CONFIGS[name][7] if len(CONFIGS[name]) > 7 else 128
         t0 = time.time()
         mesh = generate_mesh(family, dims, seed=0, dtype=dtype)
         kernel = kernel_for_mesh(kname, mesh)
         inc = INC[kname]
         m = next(iter(mesh.mappings.values()))
         rec = {"family": family, "dims": list(dims), "kernel": kname, "dtype": dtype, "staging": staging,
-               "seed": 0, "block_size": 128, "layout": "aos", "n_elements": int(m.from_set.size),
+               "seed": 0, "block_size": bs, "layout": "aos", "n_elements": int(m.from_set.size),
                "n_points": int(m.to_set.size)}
         serial = mp.execute_serial(mesh, kernel).data[inc].view2d()
         rec["serial"] = crc(serial)
@@ -119,7 +123,7 @@ def main(names):
         plans = {}
         for strategy, reorder in strategies:
             t1 = time.time()
-            cfg = mp.PlanConfig(strategy=strategy, reorder=reorder, layout="aos", staging=staging, block_size=128)
+            cfg = mp.PlanConfig(strategy=strategy, reorder=reorder, layout="aos", staging=staging, block_size=bs)
             build = mp.build_global_plan if strategy == "global" else mp.build_hierarchical_plan
             src = rmesh if (strategy, reorder) in rand_runs else mesh
             plan = build(src, kernel, cfg)

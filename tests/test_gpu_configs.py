@@ -191,11 +191,19 @@ def test_c4_headline_plan_and_loop():
         pytest.skip("no C4 fingerprint")
     rec, mesh, kernel = config_mesh("C4", lean=True)
     inc = INC_OF[rec["kernel"]]
-    plan = build(rec, mesh, kernel, "hier/partition")
-    for sched in ("pipelined-pull", "stream-pull", "stream"):
-        assert crc(run_restored(plan, kernel, inc, sched)) == FP["C4"]["serial"], sched
-    del plan
-    torch.cuda.empty_cache()
+    m = next(iter(mesh.mappings.values()))
+    # the reference's k-way plan at block 128 and at 256 (the bench headline)
+    for name in ("C4", "C4k256"):
+        if name not in FP:
+            continue
+        plan = build(FP[name], mesh, kernel, "hier/partition")
+        if "hier/partition" in FP[name].get("plans", {}):
+            bad = plan_mismatches(plan, m, FP[name]["plans"]["hier/partition"])
+            assert not bad, f"{name} k-way plan differs from the reference: {bad}"
+        for sched in ("pipelined-pull", "stream-pull", "stream"):
+            assert crc(run_restored(plan, kernel, inc, sched)) == FP["C4"]["serial"], (name, sched)
+        del plan
+        torch.cuda.empty_cache()
     cfg = mp.PlanConfig(reorder="structured:4,4,8", layout="aos", staging=rec["staging"], block_size=480)
     splan = mp.build_hierarchical_plan(mesh, kernel, cfg)
     for sched in ("stream-pull", "stream"):

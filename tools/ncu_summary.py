@@ -82,9 +82,12 @@ def launches(path: str) -> str:
         a = agg.setdefault((name, r[im], r[iu]), [0, 0.0])
         a[0] += 1
         a[1] += float(r[iv].replace(",", ""))
-    out = [f"## launch list {path}\n", "| kernel | metric | launches | total |", "|---|---|---|---|"]
+    out = [f"## launch list {path}\n", "| kernel | metric | launches | sum over launches (mean for % / ratios) |",
+           "|---|---|---|---|"]
     for (name, metric, unit), (cnt, tot) in sorted(agg.items()):
-        out.append(f"| `{name}` | {metric} | {cnt} | {tot:.4g} {unit} |")
+        rate = unit.strip() in ("%", "") or metric.endswith((".pct", ".ratio")) or "pct_of_peak" in metric
+        val = f"mean {tot / cnt:.4g}" if rate else f"{tot:.4g}"
+        out.append(f"| `{name}` | {metric} | {cnt} | {val} {unit} |")
     return "\n".join(out) + "\n"
 
 
