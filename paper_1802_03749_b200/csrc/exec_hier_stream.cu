@@ -101,6 +101,7 @@ struct StreamView {
   int32_t nt;     // compute threads (multiple of 32)
   int32_t depth;  // blocks in flight; stages = depth + 1
   int32_t stage_reads;
+  int32_t bulk_rows;  // TMA path: per-lane 1D bulk copies of 32-byte rows instead of tensor gather4
   uint32_t* stats;  // optional (MESHPLAN_STREAM_STATS): [0] late blocks
 };
 
@@ -168,6 +169,14 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, i
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(saddr(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(saddr(bar))
+      : "memory");
+}
+
+// one contiguous global -> shared copy through the TMA unit, completing on `bar`
+__device__ __forceinline__ void tma_bulk(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
       : "memory");
 }
 
@@ -471,7 +480,36 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
         if (!TMAQ && stage_reads) gather_row<T, RCN, LAYOUT>(st + L.q, j, v.ind, p, v.ind_comps, v.npts);
       }
     }
-    if constexpr (TMAQ) {
+    if constexpr (TMAQ) if (H.bulk_rows) {
+      // every lane copies its own 32-byte rows with 1D bulk copies through the
+      // TMA unit (no LSU instructions): one copy per row, or its two 16-byte
+      // granules swapped where the row format's XOR swizzle exchanges them
+      const int lane = t & 31;
+      unsigned nrow = 0;
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        const int left = ns - ((t & ~31) + r * NT);
+        nrow += left <= 0 ? 0u : (unsigned)(left > 32 ? 32 : left);
+      }
+      if (lane == 0) mbar_arrive_expect(qbar + s, nrow * (unsigned)L_t::QB);
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        const int j = t + r * NT;
+        if (j < ns) {
+          const unsigned char* src = reinterpret_cast<const unsigned char*>(v.ind + (int64_t)ids[r] * v.ind_comps);
+          unsigned char* row = st + L.q;
+          using F = RowFmt<L_t::QB>;
+          if (F::slot(j, 0) == j * F::PITCH) {
+            tma_bulk(row + F::slot(j, 0), src, (unsigned)L_t::QB, qbar + s);
+          } else {
+#pragma unroll
+            for (int c = 0; c < F::N; ++c) tma_bulk(row + F::slot(j, c), src + c * F::G, (unsigned)F::G, qbar + s);
+          }
+        }
+      }
+    } else {
       // each warp gathers its own rows, four per lane-quad leader; rows past
       // ns repeat the warp's last valid id (the q area holds ns rounded up to
       // 4 rows).  The transaction bytes are announced before any copy issues.
@@ -811,13 +849,24 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   // B200 (C5 1.55 vs 1.39 ms; per-lane coordinates serialise through uniform
   // registers, one gather4 per 4 rows), kept as the TMA-gather variant
   static const bool env_tma = getenv("MESHPLAN_STREAM_TMA") && atoi(getenv("MESHPLAN_STREAM_TMA")) != 0;
+  // per-lane 1D bulk copies of the read rows through the TMA unit (takes the
+  // q gathers off the LSU pipe)
+  static const bool env_bulk = getenv("MESHPLAN_STREAM_BULK") && atoi(getenv("MESHPLAN_STREAM_BULK")) != 0;
   CUtensorMap qmap;
   memset(&qmap, 0, sizeof(qmap));
   bool tma = false;
+  H.bulk_rows = 0;
   if constexpr (LAYOUT == MP_AOS && (QB == 32 || QB == 64 || QB == 128)) {  // 4-row groups stay 128-B aligned
-    tma = env_tma && sr && v.n > 0 && (v.ind_comps * (int)sizeof(T)) % 16 == 0 &&
-          (reinterpret_cast<uintptr_t>(v.ind) & 15) == 0;
-    if (tma) MP_CUDA_TRY_DRV(encode_row_map(&qmap, v.ind, (int)sizeof(T), dtype_code<T>(), v.ind_comps, v.npts, Op::RC));
+    const bool rows_ok = sr && v.n > 0 && (v.ind_comps * (int)sizeof(T)) % 16 == 0 &&
+                         (reinterpret_cast<uintptr_t>(v.ind) & 15) == 0;
+    if (rows_ok && env_bulk) {
+      tma = true;
+      H.bulk_rows = 1;
+    } else {
+      tma = env_tma && rows_ok;
+      if (tma)
+        MP_CUDA_TRY_DRV(encode_row_map(&qmap, v.ind, (int)sizeof(T), dtype_code<T>(), v.ind_comps, v.npts, Op::RC));
+    }
   }
   size_t smem = 0;
   for (;; --depth) {  // shrink the ring if it does not fit

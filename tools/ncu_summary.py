@@ -29,6 +29,18 @@ METRICS = [
     ("smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio", "stall: lg throttle"),
     ("smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio", "stall: mio throttle"),
     ("smsp__inst_executed.sum", "instructions"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 LSU data-pipe wavefronts % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "shared-memory load wavefronts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum", "shared-memory store wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared-memory bank conflicts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "shared-memory bank conflicts (loads)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "shared-memory bank conflicts (stores)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ldgsts.sum", "shared-memory bank conflicts (LDGSTS fills)"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 sector hit rate"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "global load requests"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_st.sum", "global store requests"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
 ]
 
 
