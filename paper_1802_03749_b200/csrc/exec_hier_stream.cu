@@ -102,6 +102,7 @@ struct StreamView {
   int32_t depth;  // blocks in flight; stages = depth + 1
   int32_t stage_reads;
   int32_t bulk_rows;  // TMA path: per-lane 1D bulk copies of 32-byte rows instead of tensor gather4
+  int32_t recompute;  // pull form: each row owner recomputes its refs' element outputs (no parking)
   uint32_t* stats;  // optional (MESHPLAN_STREAM_STATS): [0] late blocks
 };
 
@@ -637,7 +638,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
     int ls[A];
     int my_tc = -1;
     unsigned fmask = 0;  // slots whose row this element writes first (store, no load)
-    if (t < k) {
+    if (t < k && !(PULL && H.recompute)) {
       const unsigned char* em = st + L.em + t * H.em_bytes;
       const SlotT* sl = reinterpret_cast<const SlotT*>(em);
 #pragma unroll
@@ -659,11 +660,34 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
       //     in thread-colour order starting from 0 -- the reference's zeroed
       //     shared row + per-colour np.add.at (simulator.py:634-643), bit for
       //     bit -- and writes row + sum back once.
-      if (t < k) {
+      if (!H.recompute) {
+        if (t < k) {
 #pragma unroll
-        for (int q = 0; q < A; ++q) sts_row<T, IC>(sh_inc, t * A + q, o[q]);
+          for (int q = 0; q < A; ++q) sts_row<T, IC>(sh_inc, t * A + q, o[q]);
+        }
+        cbar();
       }
-      cbar();
+      // recompute form: the output of ref (element e, slot s), straight from the
+      // element's staged inputs -- the same operation on the same operands as
+      // the element's own evaluation (--fmad=false), so bit-identical
+      auto ref_out = [&](int ref, T (&x)[IC]) {
+        const int e = ref / A, sq = ref - e * A;
+        const SlotT* sl = reinterpret_cast<const SlotT*>(st + L.em + e * H.em_bytes);
+        T dd[DC], rr_[A][RCN], oo[A][IC];
+#pragma unroll
+        for (int c = 0; c < DC; ++c) dd[c] = reinterpret_cast<const T*>(st + L.dir)[c * H.max_block + e];
+        if (RC > 0 && stage_reads) {
+#pragma unroll
+          for (int q = 0; q < A; ++q) lds_row<T, RCN>(st + L.q, sl[q], rr_[q]);
+        }
+        compute<Op, T>(v, rr_, dd, oo);
+#pragma unroll
+        for (int q = 0; q < A; ++q)
+          if (q == sq) {
+#pragma unroll
+            for (int c = 0; c < IC; ++c) x[c] = oo[q][c];
+          }
+      };
       const int dl = hdr[3];
       const uint16_t* po = reinterpret_cast<const uint16_t*>(st + L.poff) + (dl & 0xffff);
       const uint16_t* pr = reinterpret_cast<const uint16_t*>(st + L.pref) + (dl >> 16);
@@ -677,11 +701,13 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
           const int64_t p = reinterpret_cast<const int*>(st + L.ids)[j];
           const int lo = po[j], hi = po[j + 1];
           T acc[IC], x[IC];
-          lds_row<T, IC>(sh_inc, pr[lo], x);
+          if (H.recompute) ref_out(pr[lo], x);
+          else lds_row<T, IC>(sh_inc, pr[lo], x);
 #pragma unroll
           for (int c = 0; c < IC; ++c) acc[c] = x[c] + T(0);  // 0 + x
           for (int rr = lo + 1; rr < hi; ++rr) {
-            lds_row<T, IC>(sh_inc, pr[rr], x);
+            if (H.recompute) ref_out(pr[rr], x);
+            else lds_row<T, IC>(sh_inc, pr[rr], x);
 #pragma unroll
             for (int c = 0; c < IC; ++c) acc[c] += x[c];
           }
@@ -852,6 +878,8 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   // per-lane 1D bulk copies of the read rows through the TMA unit (takes the
   // q gathers off the LSU pipe)
   static const bool env_bulk = getenv("MESHPLAN_STREAM_BULK") && atoi(getenv("MESHPLAN_STREAM_BULK")) != 0;
+  static const bool env_recompute = getenv("MESHPLAN_PULL_RECOMPUTE") && atoi(getenv("MESHPLAN_PULL_RECOMPUTE")) != 0;
+  H.recompute = pull && env_recompute && (Op::RC == 0 || P.stage_reads) ? 1 : 0;
   CUtensorMap qmap;
   memset(&qmap, 0, sizeof(qmap));
   bool tma = false;
