@@ -182,6 +182,16 @@ mp_status mp_exec_atomic(const mp_loop* loop, void* stream);
 mp_status mp_exec_serial(const mp_loop* loop, const int32_t* inv_offsets, const int32_t* inv_refs, void* temp,
                          void* stream);
 
+/* Hierarchical executor, gather form (colour schedule, one launch per block
+ * colour): lanes own (element, slot) refs instead of elements; each row's
+ * refs are summed in thread-colour order by a shuffle chain and written back
+ * once -- bit-identical to mp_exec_hier_stream and execute_hierarchical
+ * (simulator.py:525-656) on the same plan, without the thread-colour loop.
+ * ref_offsets / refs from mp_plan_gather_refs; max_refs = the widest block's
+ * position count.  AoS indirect arrays, staged reads. */
+mp_status mp_exec_hier_gather(const mp_loop* loop, const mp_hier_plan* plan, const int32_t* ref_offsets,
+                              const uint32_t* refs, int32_t max_refs, void* stream);
+
 /* ---- multi-GPU halo (owner compute; no reference counterpart) ----- */
 /* dst[r*comps + c] = src[rows[r]*comps + c]  (pack rows a peer imports)      */
 mp_status mp_halo_pack(int32_t dtype, const void* src, const int32_t* rows, int64_t nrows, int32_t comps, void* dst,
@@ -243,6 +253,14 @@ mp_status mp_plan_local_slots(int32_t nb, const int32_t* block_offsets, const in
 mp_status mp_plan_thread_colours(int32_t nb, const int32_t* block_offsets, const int32_t* map, int64_t n_elems,
                                  int32_t arity, int32_t map_layout, uint32_t written_mask, int32_t max_block,
                                  int32_t* colours, int32_t* counts, int32_t* sorted_order, void* stream);
+
+/* Gather-form ref records (see mp_exec_hier_gather): pass 1 (refs == NULL)
+ * writes per-block position counts; the caller scans them into ref_offsets
+ * [nb+1], fills refs with 0xFF bytes and calls again.  Built from the plan's
+ * pull lists (mp_hier_plan.pull_off / pull_ref). */
+mp_status mp_plan_gather_refs(int32_t nb, const int32_t* block_offsets, const int32_t* staged_offsets,
+                              const uint16_t* pull_off, const uint16_t* pull_ref, int32_t arity,
+                              const int32_t* ref_offsets, int32_t* counts, uint32_t* refs, void* stream);
 
 /* Executor layout of each block's staged rows (not part of the plan):
  * perm[staged_offsets[b] + position] = staged index placed at that shared

@@ -73,6 +73,8 @@ _SIGNATURES = {
     "mp_plan_block_points": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_i32, c_u32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "mp_plan_local_slots": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_i32, c_u32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mp_plan_thread_colours": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_i32, c_u32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "mp_plan_gather_refs": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "mp_exec_hier_gather": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_vp, c_vp, c_i32, c_vp]),
     "mp_plan_row_placement": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "mp_plan_block_colours": (c_i32, [c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "mp_greedy_colour_csr": (c_i32, [c_i64, c_vp, c_vp, c_i64, c_i32, c_vp]),

@@ -316,6 +316,45 @@ __global__ void row_placement_kernel(int32_t nb, const int32_t* __restrict__ bo,
     perm[s0 + c + 8 * idx[c]++] = r;
   }
 }
+
+// ---- gather-form ref records (exec_hier_gather.cu) ----------------------------
+// Per block, the pull lists' (element, slot) refs of each staged row (thread-
+// colour order) laid out row after row, a row never straddling a 32-lane
+// window (padding positions stay 0xFFFFFFFF).  Record: element (10 bits), own
+// row (10), slot (3), position in the row's run (5), run end (1).  Pass 1
+// (rec == NULL) counts positions per block (rounded up to 4).
+__global__ void gather_refs_kernel(int32_t nb, const int32_t* __restrict__ bo, const int32_t* __restrict__ st_off,
+                                   const uint16_t* __restrict__ poff, const uint16_t* __restrict__ pref, int arity,
+                                   const int32_t* __restrict__ roff, int32_t* counts, uint32_t* rec, int* bad) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const int e0 = bo[b], s0 = st_off[b], ns = st_off[b + 1] - s0;
+  const uint16_t* po = poff + s0 + b;
+  const uint16_t* pr = pref + (int64_t)e0 * arity;
+  int pos = 0;
+  for (int j = 0; j < ns; ++j) {
+    const int lo = po[j], len = (int)po[j + 1] - lo;
+    if (len <= 0) continue;
+    if (len > 32 || j > 1023) {
+      atomicMin(bad, b);
+      return;
+    }
+    if ((pos & 31) + len > 32) pos = (pos + 31) & ~31;
+    if (rec) {
+      for (int q = 0; q < len; ++q) {
+        const int ref = pr[lo + q], e = ref / arity, sl = ref - e * arity;
+        if (e > 1022) {
+          atomicMin(bad, b);
+          return;
+        }
+        rec[roff[b] + pos + q] = (uint32_t)e | (uint32_t)j << 10 | (uint32_t)sl << 20 | (uint32_t)q << 23 |
+                                 (uint32_t)(q == len - 1) << 28;
+      }
+    }
+    pos += len;
+  }
+  if (!rec) counts[b] = (pos + 3) & ~3;
+}
 }  // namespace
 }  // namespace mp
 
@@ -395,5 +434,27 @@ extern "C" mp_status mp_plan_row_placement(int32_t nb, const int32_t* block_offs
   mp::row_placement_kernel<<<(nb + 127) / 128, 128, 0, as_stream(stream)>>>(nb, block_offsets, staged_offsets,
                                                                             local_slots, arity, thread_colours, perm);
   MP_CHECK_LAUNCH();
+  return MP_OK;
+}
+
+extern "C" mp_status mp_plan_gather_refs(int32_t nb, const int32_t* block_offsets, const int32_t* staged_offsets,
+                                        const uint16_t* pull_off, const uint16_t* pull_ref, int32_t arity,
+                                        const int32_t* ref_offsets, int32_t* counts, uint32_t* refs, void* stream) {
+  clear_error();
+  if (nb == 0) return MP_OK;
+  cudaStream_t st = as_stream(stream);
+  int* d_bad = nullptr;
+  MP_CUDA_TRY(cudaMallocAsync(&d_bad, sizeof(int), st));
+  int big = INT_MAX;
+  MP_CUDA_TRY(cudaMemcpyAsync(d_bad, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  mp::gather_refs_kernel<<<(nb + 127) / 128, 128, 0, st>>>(nb, block_offsets, staged_offsets, pull_off, pull_ref,
+                                                            arity, ref_offsets, counts, refs, d_bad);
+  MP_CHECK_LAUNCH();
+  int bad = INT_MAX;
+  MP_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MP_CUDA_TRY(cudaFreeAsync(d_bad, st));
+  MP_CUDA_TRY(cudaStreamSynchronize(st));
+  if (bad != INT_MAX)
+    MP_FAIL(MP_ERR_CAPACITY, "block %d: gather records need <= 32 refs per row, <= 1024 rows, <= 1023 elements", bad);
   return MP_OK;
 }

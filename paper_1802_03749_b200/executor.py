@@ -35,6 +35,9 @@ SCHEDULES = {
     "stream": (_native.MP_SCHED_COLOUR, "stream"),
     "stream-dataflow": (_native.MP_SCHED_DATAFLOW, "stream"),
     "stream-pull": (_native.MP_SCHED_COLOUR | _native.MP_SCHED_PULL, "stream"),
+    # gather form (exec_hier_gather.cu): lanes own (element, slot) refs, each
+    # row's run summed in thread-colour order by a shuffle chain; no colour loop
+    "gather": (_native.MP_SCHED_COLOUR, "gather"),
     # comparison baseline (not bit-exact: atomics reassociate): ignores the colouring
     "atomic": (_native.MP_SCHED_COLOUR, "atomic"),
     # comparison baseline (the paper's temporary-array strategy; bit-identical
@@ -256,6 +259,11 @@ class DeviceLoop:
         that view's blocks."""
         sp = _native.stream_ptr(stream)
         dp = self.plan._device
+        if self.pipelined == "gather":
+            roff, refs, max_refs = dp.gather_refs()
+            _native.call("mp_exec_hier_gather", self.loop, (sub.struct if sub is not None else dp.struct_cached()),
+                         _native.ptr(roff), _native.ptr(refs), int(max_refs), sp)
+            return
         if sub is not None:
             if isinstance(self.plan, GlobalPlan) or self.pipelined in ("atomic", "temp-array") or \
                     self.schedule & 3 == _native.MP_SCHED_DATAFLOW:
@@ -607,6 +615,7 @@ def _report(plan, kernel, loop: DeviceLoop, ms: float | None) -> MetricsReport:
         "hier", n, loop.launches_per_run(), plan.block_colours.num_colours, ub, tb, ops, occ, bps,
         reuse_factor(plan), int(plan.thread_colour_counts.max()) if nb else 0,
         float(plan.thread_colour_counts.mean()) if nb else 0.0, int(sync.sum()) if nb else 0, sync, smax, nb,
+        "gather" if loop.pipelined == "gather" else
         ("stream-" if loop.pipelined == "stream" else "pipelined-" if loop.pipelined else "") + ("dataflow" if loop.schedule & 3 == _native.MP_SCHED_DATAFLOW
                                                     else "colour") + ("-pull" if loop.schedule & 4 else ""),
         ms, gbps,

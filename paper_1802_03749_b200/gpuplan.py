@@ -511,6 +511,32 @@ class DevicePlan:
         p.tblock_colour = bbc.data_ptr()
         return SubPlan(p, int(idx.numel()), int(np.count_nonzero(np.diff(sub_offs))), [bbc, tdesc, sub_offs])
 
+    def gather_refs(self):
+        """Ref records of the gather-form executor (``mp_plan_gather_refs``),
+        built once from the pull lists: (ref offsets [nb+1], records, widest
+        block's position count)."""
+        cached = self.__dict__.get("_gather")
+        if cached is not None:
+            return cached
+        if self.pull_off is None or self.pull_ref is None:
+            raise KernelSpecError("the gather form needs pull lists: every slot staged and written")
+        nb = self.block_offsets.numel() - 1
+        dev = self.block_offsets.device
+        arity = self.map.shape[1]
+        counts = torch.zeros(max(nb, 1), dtype=torch.int32, device=dev)
+        args = (nb, _native.ptr(self.block_offsets), _native.ptr(self.staged_off), _native.ptr(self.pull_off),
+                _native.ptr(self.pull_ref), int(arity))
+        _native.call("mp_plan_gather_refs", *args, None, _native.ptr(counts), None, _sp())
+        roff = torch.zeros(nb + 1, dtype=torch.int32, device=dev)
+        if nb:
+            roff[1:] = torch.cumsum(counts[:nb], 0, dtype=torch.int32)
+        total = int(roff[-1])
+        refs = torch.full((max(total, 1),), -1, dtype=torch.int32, device=dev)
+        _native.call("mp_plan_gather_refs", *args, _native.ptr(roff), _native.ptr(counts), _native.ptr(refs), _sp())
+        max_refs = int(counts[:nb].max()) if nb else 0
+        self.__dict__["_gather"] = (roff, refs, max_refs)
+        return self.__dict__["_gather"]
+
     def reschedule(self, lag: int) -> None:
         """Recompute the dataflow order for another lag (tuning)."""
         ncol = len(self.colour_block_offsets) - 1
