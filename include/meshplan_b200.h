@@ -182,6 +182,16 @@ mp_status mp_exec_atomic(const mp_loop* loop, void* stream);
 mp_status mp_exec_serial(const mp_loop* loop, const int32_t* inv_offsets, const int32_t* inv_refs, void* temp,
                          void* stream);
 
+/* mp_exec_hier_stream (colour schedules) with the multi-GPU halo export
+ * fused into the write-back: export_dest[staged entry] = (peer << 24 | row)
+ * for the halo rows whose block is their last writer (-1 elsewhere); that
+ * block also stores the row's final value into row `row` of
+ * peer_slots[peer] + (epoch & 1) * slot_strides[peer] (the owner's mailbox
+ * slot, IPC-mapped: P2P stores over NVLink).  *epoch is read on the device. */
+mp_status mp_exec_hier_stream_export(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule,
+                                     const int32_t* export_dest, int32_t npeers, void* const* peer_slots,
+                                     const int64_t* slot_strides, const uint32_t* epoch, void* stream);
+
 /* Hierarchical executor, gather form (colour schedule, one launch per block
  * colour): lanes own (element, slot) refs instead of elements; each row's
  * refs are summed in thread-colour order by a shuffle chain and written back
@@ -214,6 +224,9 @@ mp_status mp_halo_put(int32_t dtype, const void* src, const int32_t* rows, int64
 mp_status mp_halo_get(int32_t dtype, void* dst, const int32_t* rows, int64_t nrows, int32_t comps, const void* mailbox,
                       int64_t slot_elems, const uint32_t* flag, const uint32_t* epoch, int32_t mode, void* stream);
 mp_status mp_epoch_bump(uint32_t* epoch, void* stream);
+/* Release the step epoch into a peer's flag after this stream's earlier work
+ * (the fused export's P2P row stores) -- the put without the copy. */
+mp_status mp_halo_signal(uint32_t* remote_flag, const uint32_t* epoch, void* stream);
 /* Zeroed device allocation (cudaMalloc: IPC-exportable; free with mp_free),
  * its 64-byte IPC handle, and a peer process's mapping of one (closed with
  * mp_ipc_close). */

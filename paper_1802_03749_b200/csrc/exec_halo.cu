@@ -97,6 +97,13 @@ __global__ void halo_get_kernel(T* dst, const int32_t* __restrict__ rows, int64_
 
 __global__ void epoch_bump_kernel(uint32_t* epoch) { *epoch += 1u; }
 
+// the previous kernels on this stream have completed (stream order); make
+// their P2P stores visible system-wide before the flag
+__global__ void halo_signal_kernel(uint32_t* remote_flag, const uint32_t* epoch_p) {
+  __threadfence_system();
+  st_release_sys(remote_flag, *epoch_p);
+}
+
 inline int grid_of(int64_t n) {
   int64_t g = (n + 255) / 256;
   return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
@@ -208,5 +215,12 @@ extern "C" mp_status mp_ipc_open(const unsigned char* handle, void** ptr) {
 extern "C" mp_status mp_ipc_close(void* ptr) {
   mp::clear_error();
   MP_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return MP_OK;
+}
+
+extern "C" mp_status mp_halo_signal(uint32_t* remote_flag, const uint32_t* epoch, void* stream) {
+  mp::clear_error();
+  mp::halo_signal_kernel<<<1, 1, 0, mp::as_stream(stream)>>>(remote_flag, epoch);
+  MP_CHECK_LAUNCH();
   return MP_OK;
 }

@@ -103,6 +103,14 @@ struct StreamView {
   int32_t stage_reads;
   int32_t bulk_rows;  // TMA path: per-lane 1D bulk copies of 32-byte rows instead of tensor gather4
   int32_t recompute;  // pull form: each row owner recomputes its refs' element outputs (no parking)
+  // fused halo export (multi-GPU, colour schedules): staged entry -> (owner
+  // peer << 24 | row of the owner's mailbox slot), -1 = none; the block that
+  // writes a halo row last also stores the row's final value into the owner's
+  // mailbox (P2P) in its write-back
+  const int32_t* export_dest;
+  unsigned char* export_base[8];   // per peer: the owner's export slot for this rank (parity 0)
+  int64_t export_stride[8];        // bytes between the two parity slots
+  const uint32_t* epoch_ptr;
   uint32_t* stats;  // optional (MESHPLAN_STREAM_STATS): [0] late blocks
 };
 
@@ -471,6 +479,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
       hdr[0] = k;
       hdr[1] = ns;
       hdr[2] = d.y >> 16;
+      ctl[2 + s] = d.z;  // staged offset of the stage's block (fused export)
     }
 #pragma unroll
     for (int r = 0; r < MAXR; ++r) {
@@ -558,6 +567,17 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
   };
   // increment rows of block f (staged ids of stage s) -> registers; on the
   // dataflow schedule only once the block's predecessors are known done
+  const uint32_t xpar = H.export_dest ? (__ldg(H.epoch_ptr) & 1u) : 0u;
+  // fused halo export: a halo row's last writer also stores the final value
+  // into the owner's mailbox slot (256-bit P2P store for 32-byte rows)
+  auto export_row = [&](int s_, int j, const T (&val)[IC]) {
+    if (H.export_dest == nullptr) return;
+    const int dst = __ldg(H.export_dest + ctl[2 + s_] + j);
+    if (dst < 0) return;
+    const int peer = dst >> 24;
+    T* remote = reinterpret_cast<T*>(H.export_base[peer] + xpar * H.export_stride[peer]);
+    stg_row<T, IC, MP_AOS>(remote, dst & 0xFFFFFF, 0, val);
+  };
   T rrow[MAXR][IC];
   bool rows_late = false;
   auto load_rows = [&](int f, int s) {
@@ -715,6 +735,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
 #pragma unroll
           for (int c = 0; c < IC; ++c) acc[c] = rrow[r][c] + acc[c];
           stg_row<T, IC, LAYOUT>(v.inc, p, v.npts, acc);
+          export_row(s, j, acc);
         }
       }
     } else {
@@ -754,6 +775,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
 #pragma unroll
         for (int c = 0; c < IC; ++c) acc[c] = rrow[r][c] + acc[c];
         stg_row<T, IC, LAYOUT>(v.inc, p, v.npts, acc);
+        export_row(s, j, acc);
       }
     }
     }  // push form
@@ -1004,9 +1026,17 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   return MP_OK;
 }
 
+struct ExportArgs {
+  const int32_t* dest;
+  int32_t npeers;
+  void* const* bases;
+  const int64_t* strides;
+  const uint32_t* epoch;
+};
+
 template <class Op, typename T>
 mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool dataflow, bool pull, uint32_t epoch,
-                           cudaStream_t st) {
+                           cudaStream_t st, const ExportArgs* ex = nullptr) {
   if constexpr (!op_supported<Op, T>()) {
     MP_FAIL(MP_ERR_KERNEL, "heavy face flux needs float data");
   } else {
@@ -1031,6 +1061,17 @@ mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool datafl
     H.flags = P.flags;
     H.epoch = epoch;
     H.em_bytes = P.elem_meta_bytes;
+    if (ex && ex->dest) {
+      if (dataflow) MP_FAIL(MP_ERR_KERNEL, "fused halo export runs under the colour schedules");
+      if (Lp.ind_layout != MP_AOS) MP_FAIL(MP_ERR_KERNEL, "fused halo export needs AoS increment rows");
+      if (ex->npeers < 0 || ex->npeers > 8) MP_FAIL(MP_ERR_KERNEL, "fused halo export: %d peers (max 8)", ex->npeers);
+      H.export_dest = ex->dest;
+      for (int q = 0; q < ex->npeers; ++q) {
+        H.export_base[q] = static_cast<unsigned char*>(ex->bases[q]);
+        H.export_stride[q] = ex->strides[q];
+      }
+      H.epoch_ptr = ex->epoch;
+    }
     LoopView<T> v = make_view<T>(Lp);
     const bool u8 = P.slot_bytes == 1;
     if (Lp.ind_layout == MP_AOS) {
@@ -1059,5 +1100,24 @@ extern "C" mp_status mp_exec_hier_stream(const mp_loop* loop, const mp_hier_plan
   const mp_hier_plan& P = *plan;
   return MP_DISPATCH_OP(L.op, [&]() {
     return MP_DISPATCH_DTYPE(L.dtype, [&]() { return mp::launch_stream_op<Op, scalar_t>(L, P, df, pull, epoch, st); });
+  });
+}
+
+extern "C" mp_status mp_exec_hier_stream_export(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule,
+                                                const int32_t* export_dest, int32_t npeers, void* const* peer_slots,
+                                                const int64_t* slot_strides, const uint32_t* epoch, void* stream) {
+  mp::clear_error();
+  if (!loop || !plan || !export_dest || !epoch || (npeers > 0 && (!peer_slots || !slot_strides)))
+    MP_FAIL(MP_ERR_KERNEL, "null argument");
+  if ((schedule & 3) == MP_SCHED_DATAFLOW) MP_FAIL(MP_ERR_KERNEL, "fused halo export runs under the colour schedules");
+  const bool pull = (schedule & MP_SCHED_PULL) != 0;
+  if (pull && plan->num_blocks > 0 && (!plan->pull_off || !plan->pull_ref))
+    MP_FAIL(MP_ERR_KERNEL, "pull form needs the plan's pull lists");
+  cudaStream_t st = mp::as_stream(stream);
+  const mp::ExportArgs ex{export_dest, npeers, peer_slots, slot_strides, epoch};
+  const mp_loop& L = *loop;
+  const mp_hier_plan& P = *plan;
+  return MP_DISPATCH_OP(L.op, [&]() {
+    return MP_DISPATCH_DTYPE(L.dtype, [&]() { return mp::launch_stream_op<Op, scalar_t>(L, P, false, pull, 0, st, &ex); });
   });
 }

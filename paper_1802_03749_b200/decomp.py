@@ -260,7 +260,8 @@ class PeerExchange:
     ``publish(ptr, layout, needed)`` exchanges mailboxes (``PeerHub`` for
     threads, ``ipc_connector`` for processes)."""
 
-    def __init__(self, dec: Decomposition, publish, device, dtype: torch.dtype, read_comps: int, inc_comps: int):
+    def __init__(self, dec: Decomposition, publish, device, dtype: torch.dtype, read_comps: int, inc_comps: int,
+                 fused_export: bool = False):
         self.dec, self.dev, self.dtype = dec, torch.device(device), dtype
         self.mp_dtype = TORCH_TO_MP[dtype]
         item = torch.empty(0, dtype=dtype).element_size()
@@ -290,6 +291,15 @@ class PeerExchange:
         self.peers = publish(self.base, layout, needed)  # every rank takes part (a collective)
         self._ipc = getattr(publish, "ipc", False)
         self._opened = [v[0] for v in self.peers.values()] if self._ipc else []
+        # fused export: the loop's write-back stores each halo row's final value
+        # into its owner's slot; the exchange only signals (mp_halo_signal)
+        self.fused = bool(fused_export)
+        self.owners = sorted(dec.halo_rows)
+        self.export_slots = []   # per owner index: (slot base address, parity stride in bytes)
+        for p in self.owners:
+            pbase, play = self.peers[p]
+            off, n = play[f"exp:{dec.rank}"]
+            self.export_slots.append((pbase + off, max(n, 1) * item))
 
     def _flag(self, base: int, layout: dict, sender: int, d: int) -> int:
         return base + layout["flags"] + (sender * 2 + d) * 4
@@ -322,7 +332,12 @@ class PeerExchange:
 
     def export_increments(self, arr: torch.Tensor, comps: int) -> None:
         for peer, rows in self.halo.items():
-            self._put(arr, rows, comps, peer, 1)
+            if self.fused:  # rows already stored by the loop's write-back
+                pbase, play = self.peers[peer]
+                _native.call("mp_halo_signal", self._flag(pbase, play, self.dec.rank, 1), self.epoch_ptr,
+                             _native.stream_ptr())
+            else:
+                self._put(arr, rows, comps, peer, 1)
         for peer, rows in self.exports.items():
             self._get(arr, rows, comps, peer, 1, ADD)
         if self.all_halo is not None:
@@ -354,7 +369,7 @@ class DistributedLoop:
     """One rank's share of a decomposed flux-type loop: local plan + halo."""
 
     def __init__(self, mesh_local, kernel, dec: Decomposition, transport, config, schedule="stream",
-                 overlap=None):
+                 overlap=None, fused_export=None):
         import paper_1802_03749_b200 as mp
 
         self.plan = mp.build_hierarchical_plan(mesh_local, kernel, config)
@@ -369,11 +384,26 @@ class DistributedLoop:
         # peer-memory exchange (device-side, graph-capturable); otherwise host-driven
         # send/recv through the given transport
         self.peer = hasattr(transport, "ipc")
+        # fused export (SURVEY 8e step two): the streamed colour executor's
+        # write-back stores each halo row's final value straight into its
+        # owner's mailbox (P2P); needs the peer exchange and AoS rows
+        # (an import round each step orders a sender's slot reuse after the
+        # owner's read of it, so the fused export needs an indirectly read array)
+        stream_colour = schedule in ("stream", "stream-pull") and self.read is not None
+        if fused_export is None:
+            fused_export = self.peer and stream_colour
+        if fused_export and not (self.peer and stream_colour):
+            raise ValueError("fused export needs the peer exchange, a streamed colour schedule and an indirect read")
         if self.peer:
             self.halo = PeerExchange(self.dec, transport, "cuda", self.loop.tensors[self.inc].dtype,
-                                     self.rc or 0, self.ic)
+                                     self.rc or 0, self.ic, fused_export=fused_export)
         else:
             self.halo = HaloExchange(self.dec, transport, "cuda")
+        self.fused = bool(fused_export)
+        if self.fused:
+            self.export_dest = self._export_dest()
+            self._ex_bases = (ctypes.c_void_p * 8)(*[b for b, _ in self.halo.export_slots])
+            self._ex_strides = (ctypes.c_int64 * 8)(*[st for _, st in self.halo.export_slots])
         # core / boundary split: core blocks touch no halo point, so
         # they run while the halo import is in flight; the colour schedules only
         if overlap is None:
@@ -384,6 +414,45 @@ class DistributedLoop:
             self.core = self.plan._device.subset(core)
             self.boundary = self.plan._device.subset(~core)
             self.comm = torch.cuda.Stream()
+
+    def _export_dest(self) -> torch.Tensor:
+        """Per staged entry of the local plan: (owner index << 24 | row in the
+        owner's export slot) where the entry's block is the last writer (the
+        highest block colour) of a halo row, else -1."""
+        dp = self.plan._device
+        dev = dp.staged_ids.device
+        st_off = dp.staged_off.long()
+        total = int(st_off[-1])
+        ids = dp.staged_ids[:total].long()
+        nb = st_off.numel() - 1
+        blk = torch.repeat_interleave(torch.arange(nb, device=dev), st_off[1:] - st_off[:-1])
+        colour = dp.block_colours.long()[blk]
+        n_local = self.dec.n_local
+        hpeer = torch.full((n_local,), -1, dtype=torch.long, device=dev)
+        hpos = torch.zeros(n_local, dtype=torch.long, device=dev)
+        for q, p in enumerate(self.halo.owners):
+            rows = torch.as_tensor(np.asarray(self.dec.halo_rows[p], dtype=np.int64), device=dev)
+            if q > 255 or rows.numel() >= 1 << 24:
+                raise ValueError("fused export: too many owners or halo rows")
+            hpeer[rows] = q
+            hpos[rows] = torch.arange(rows.numel(), device=dev)
+        dest = torch.full((max(total, 1) + 4,), -1, dtype=torch.int32, device=dev)
+        halo = hpeer[ids] >= 0
+        if bool(halo.any()):
+            last = torch.full((n_local,), -1, dtype=torch.long, device=dev)
+            last.scatter_reduce_(0, ids[halo], colour[halo], reduce="amax")
+            mark = halo & (colour == last[ids])
+            dest[:total][mark] = ((hpeer[ids[mark]] << 24) | hpos[ids[mark]]).to(torch.int32)
+        return dest
+
+    def _run(self, sub=None) -> None:
+        if not self.fused:
+            self.loop.run(sub=sub)
+            return
+        dp = self.plan._device
+        _native.call("mp_exec_hier_stream_export", self.loop.loop, (sub.struct if sub is not None else dp.struct_cached()),
+                     self.loop.schedule, self.export_dest.data_ptr(), len(self.halo.owners), self._ex_bases,
+                     self._ex_strides, self.halo.epoch_ptr, _native.stream_ptr())
 
     def core_blocks(self) -> torch.Tensor:
         """Per block of the local plan: true when none of its elements
@@ -407,7 +476,7 @@ class DistributedLoop:
         if self.core is None:
             if self.read is not None:
                 self.halo.import_rows(self.loop.tensors[self.read], self.rc)
-            self.loop.run()
+            self._run()
         else:
             cur = torch.cuda.current_stream()
             self.comm.wait_stream(cur)       # this step's inputs are in place
@@ -415,7 +484,7 @@ class DistributedLoop:
             with torch.cuda.stream(self.comm):
                 self.halo.import_rows(self.loop.tensors[self.read], self.rc)
             cur.wait_stream(self.comm)
-            self.loop.run(sub=self.boundary)
+            self._run(sub=self.boundary)     # the halo rows' last writers export them (fused)
         self.halo.export_increments(self.loop.tensors[self.inc], self.ic)
 
     def warmup_step(self) -> None:

@@ -212,7 +212,7 @@ def test_threaded_ranks_on_one_gpu_match_serial(world, reorder, schedule, overla
 
 
 def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, graph, barrier=lambda: None,
-               capture_lock=None):
+               capture_lock=None, fused=None):
     """One rank's share with the peer-memory exchange; returns (lo, owned rows).
     ``barrier`` separates setup from stepping: ranks sharing one device must
     not synchronise the whole device (plan building does) while a peer's
@@ -233,8 +233,9 @@ def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, gra
     local = decomp.local_flux_mesh(t, g, dec, q[dec.local_points], w[g], np.zeros((dec.n_local, 4)))
     kernel = mp.kernel_for_mesh("flux", local)
     dl = decomp.DistributedLoop(local, kernel, dec, publish, mp.PlanConfig(reorder=reorder, block_size=64),
-                                schedule, overlap=overlap)
+                                schedule, overlap=overlap, fused_export=fused)
     assert dl.peer
+    assert dl.fused == (schedule in ("stream", "stream-pull") if fused is None else fused)
     barrier()
     if graph:
         dl.warmup_step()
@@ -257,13 +258,17 @@ def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, gra
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,reorder,schedule,overlap,graph", [
-    (2, "gps", "stream", False, False), (3, "none", "stream", True, False), (4, "gps", "stream", True, True),
-    (2, "none", "colour", True, True), (3, "gps", "pipelined", False, True), (2, "gps", "stream-pull", True, True)])
-def test_peer_exchange_threads_on_one_gpu_match_serial(world, reorder, schedule, overlap, graph):
+@pytest.mark.parametrize("world,reorder,schedule,overlap,graph,fused", [
+    (2, "gps", "stream", False, False, None), (3, "none", "stream", True, False, None),
+    (4, "gps", "stream", True, True, None), (3, "gps", "stream", True, True, False),
+    (2, "none", "colour", True, True, None), (3, "gps", "pipelined", False, True, None),
+    (2, "gps", "stream-pull", True, True, None), (4, "none", "stream-pull", False, False, None)])
+def test_peer_exchange_threads_on_one_gpu_match_serial(world, reorder, schedule, overlap, graph, fused):
     """Ranks as threads on one device exchanging through each other's
     mailboxes (device pointers): direct steps and CUDA-graph replays of a
-    whole step both equal the serial loop."""
+    whole step both equal the serial loop; under the streamed colour
+    schedules the increment export is fused into the loop's write-back (the
+    halo rows' last writers store them into the owners' mailboxes)."""
     import threading
 
     nx, ny, steps = 64, 48, 3
@@ -278,7 +283,7 @@ def test_peer_exchange_threads_on_one_gpu_match_serial(world, reorder, schedule,
         try:
             with torch.cuda.stream(torch.cuda.Stream()):
                 out[r], dl = _peer_rank(r, world, nx, ny, reorder, schedule, overlap, hub.connector(r), steps, graph,
-                                        bar.wait, cap_lock)
+                                        bar.wait, cap_lock, fused)
                 loops_.append(dl)
         except Exception as exc:  # pragma: no cover - surfaced below
             errors.append(exc)
