@@ -257,56 +257,15 @@ def _peer_rank(r, world, nx, ny, reorder, schedule, overlap, publish, steps, gra
     return res, dl
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("world,reorder,schedule,overlap,graph,fused", [
-    (2, "gps", "stream", False, False, None), (3, "none", "stream", True, False, None),
-    (4, "gps", "stream", True, True, None), (3, "gps", "stream", True, True, False),
-    (2, "none", "colour", True, True, None), (3, "gps", "pipelined", False, True, None),
-    (2, "gps", "stream-pull", True, True, None), (4, "none", "stream-pull", False, False, None)])
-def test_peer_exchange_threads_on_one_gpu_match_serial(world, reorder, schedule, overlap, graph, fused):
-    """Ranks as threads on one device exchanging through each other's
-    mailboxes (device pointers): direct steps and CUDA-graph replays of a
-    whole step both equal the serial loop; under the streamed colour
-    schedules the increment export is fused into the loop's write-back (the
-    halo rows' last writers store them into the owners' mailboxes)."""
-    import threading
-
-    nx, ny, steps = 64, 48, 3
-    _, want = _global_case(nx, ny)
-    hub = decomp.PeerHub()
-    out, errors, loops_ = {}, [], []
-    bar = threading.Barrier(world, timeout=240)
-    cap_lock = threading.Lock()
-
-    def rank_main(r):
-        torch.cuda.set_device(0)
-        try:
-            with torch.cuda.stream(torch.cuda.Stream()):
-                out[r], dl = _peer_rank(r, world, nx, ny, reorder, schedule, overlap, hub.connector(r), steps, graph,
-                                        bar.wait, cap_lock, fused)
-                loops_.append(dl)
-        except Exception as exc:  # pragma: no cover - surfaced below
-            errors.append(exc)
-            bar.abort()
-
-    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
-    for th in threads:
-        th.start()
-    for th in threads:
-        th.join(timeout=300)
-    assert not errors, errors
-    full = np.zeros_like(want)
-    for lo, block in out.values():
-        full[lo: lo + block.shape[0]] = block
-    assert np.array_equal(full, steps * want)
-    torch.cuda.synchronize()
-    for dl in loops_:
-        dl.halo.close()
-
-
-def _ipc_rank_main(rank, world, port, result_file):
+def _ipc_rank_main(rank, world, port, result_file, case):
+    """One rank as its own process (gloo rendezvous, mailboxes through CUDA
+    IPC).  Ranks sharing one device must be processes: threads of one
+    process share its hardware work queues, so one rank's waiting exchange
+    kernel can stall another rank's queued put (a cross-rank deadlock that
+    separate GPUs, or separate processes time-slicing one GPU, never see)."""
     import torch.distributed as dist
 
+    nx, ny, reorder, schedule, overlap, graph, fused, steps = case
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
@@ -316,30 +275,53 @@ def _ipc_rank_main(rank, world, port, result_file):
         dist.all_gather_object(out, obj)
         return out
 
-    (lo, owned), dl = _peer_rank(rank, world, 24, 20, "gps", "stream", True, decomp.ipc_connector(allgather), 2,
-                                 graph=True, barrier=dist.barrier)
+    (lo, owned), dl = _peer_rank(rank, world, nx, ny, reorder, schedule, overlap, decomp.ipc_connector(allgather),
+                                 steps, graph=graph, barrier=dist.barrier, fused=fused)
     parts = [None] * world
     dist.all_gather_object(parts, (lo, owned))
     dist.barrier()
     dl.halo.close()
     if rank == 0:
-        _, want = _global_case(24, 20)
+        _, want = _global_case(nx, ny)
         full = np.zeros_like(want)
         for lo_, block in parts:
             full[lo_: lo_ + block.shape[0]] = block
-        np.save(result_file, np.stack([full, 2 * want]))
+        np.save(result_file, np.stack([full, steps * want]))
     dist.destroy_process_group()
 
 
+PEER_CASES = [  # world, reorder, schedule, overlap, graph, fused (None: the default, fused under stream schedules)
+    (2, "gps", "stream", False, False, None), (3, "none", "stream", True, False, None),
+    (4, "gps", "stream", True, True, None), (3, "gps", "stream", True, True, False),
+    (2, "none", "colour", True, True, None), (3, "gps", "pipelined", False, True, None),
+    (2, "gps", "stream-pull", True, True, None), (2, "none", "stream-pull", False, False, None)]
+
+
 @pytest.mark.gpu
-def test_peer_exchange_two_processes_ipc_on_one_gpu(tmp_path):
-    """Two processes (gloo rendezvous only) on one device, mailboxes mapped
-    through CUDA IPC, whole steps replayed as CUDA graphs: the path the
-    multi-GPU bench takes, with the peer on the same device instead of across
-    NVLink."""
+@pytest.mark.parametrize("world,reorder,schedule,overlap,graph,fused", PEER_CASES)
+def test_peer_exchange_processes_on_one_gpu_match_serial(world, reorder, schedule, overlap, graph, fused, tmp_path):
+    """N processes (gloo rendezvous only) on one device exchanging through
+    each other's IPC-mapped mailboxes: direct steps and CUDA-graph replays of
+    a whole step equal the serial loop; under the streamed colour schedules
+    the increment export is fused into the loop's write-back (the halo rows'
+    last writers store them into the owners' mailboxes)."""
     import torch.multiprocessing as tmp
 
     out = str(tmp_path / "full.npy")
-    tmp.spawn(_ipc_rank_main, args=(2, _free_port(), out), nprocs=2, join=True)
+    case = (32, 24, reorder, schedule, overlap, graph, fused, 3)
+    tmp.spawn(_ipc_rank_main, args=(world, _free_port(), out, case), nprocs=world, join=True)
+    got, want = np.load(out)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+def test_peer_exchange_two_processes_larger_mesh(tmp_path):
+    """The bench's configuration in miniature: two processes, GPS plans, the
+    core/boundary overlap, the fused export, graph-replayed steps."""
+    import torch.multiprocessing as tmp
+
+    out = str(tmp_path / "full.npy")
+    case = (96, 80, "gps", "stream", True, True, None, 2)
+    tmp.spawn(_ipc_rank_main, args=(2, _free_port(), out, case), nprocs=2, join=True)
     got, want = np.load(out)
     assert np.array_equal(got, want)
