@@ -561,9 +561,20 @@ def bench_rank(args, rank: int, world: int) -> int:
 
     bench = __import__("bench")
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    # MESHPLAN_RANKS_SHARE_DEVICE=1: every rank on cuda:0 with a gloo process
+    # group (rendezvous / timing collectives only; the halo data goes through
+    # the IPC-mapped mailboxes) -- the N-rank path exercised on a one-GPU box
+    shared = os.environ.get("MESHPLAN_RANKS_SHARE_DEVICE") == "1"
+    if shared and getattr(args, "transport", "peer") != "peer":
+        raise SystemExit("ranks sharing a device need the peer transport (NCCL refuses duplicate GPUs)")
+    if shared:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    dist.init_process_group("nccl", device_id=dev)
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     family, dims, kname, dtype, staging = bench.CONFIGS[args.config]
     if family != "quad2d" or kname != "flux":
         raise SystemExit("the multi-GPU bench decomposes the quad2d flux configs (C1/C5)")
@@ -630,7 +641,8 @@ def bench_rank(args, rank: int, world: int) -> int:
         torch.cuda.synchronize()
         step_ms = sum(ea.elapsed_time(eb) for ea, eb in evs) / args.steps
     dist.barrier()
-    ms = torch.tensor([step_ms], device=dev)
+    cdev = torch.device("cpu") if shared else dev  # gloo collectives take host tensors
+    ms = torch.tensor([step_ms], device=cdev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     clocks = sampler.stop()
     # end to end: pinned host copies of this rank's arrays -> H2D -> step -> D2H
@@ -650,9 +662,9 @@ def bench_rank(args, rank: int, world: int) -> int:
         dl.step_host(host, out)
     b.record()
     torch.cuda.synchronize()
-    ms_e2e = torch.tensor([a.elapsed_time(b) / n_e2e], device=dev)
+    ms_e2e = torch.tensor([a.elapsed_time(b) / n_e2e], device=cdev)
     dist.all_reduce(ms_e2e, op=dist.ReduceOp.MAX)
-    io = torch.tensor([h2d, d2h], dtype=torch.float64, device=dev)
+    io = torch.tensor([h2d, d2h], dtype=torch.float64, device=cdev)
     dist.all_reduce(io)
     n_edges = nx * (ny - 1) + ny * (nx - 1)
     ub_total = nx * ny * 4 * 8 * 3 + n_edges * (2 * 8 + 2 * 4)
@@ -669,6 +681,7 @@ def bench_rank(args, rank: int, world: int) -> int:
                            "peer-memory halo exchange (P2P puts into IPC-mapped mailboxes, device-side epoch "
                            "flags), each step one CUDA graph" if dl.peer else "NCCL halo exchange"),
                        "host_enqueue_us_per_step": round(enqueue_us, 2),
+                       "ranks_share_device": shared,
                        "useful_bytes_per_step": ub_total,
                        "l2": "inputs larger than L2 (no flush)" if flush.buf is None else "flushed between steps"},
             "roofline": {"bound": "hbm", "achieved": round(gbps / world, 2), "peak": peak, "unit": "GB/s",
