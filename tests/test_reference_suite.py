@@ -13,10 +13,10 @@ import pytest
 
 from conftest import REPO
 
-pytestmark = pytest.mark.gpu
 STAGED = REPO / "baseline" / "_ref_tests"
 
 
+@pytest.mark.gpu
 @pytest.mark.skipif(not (STAGED / "conftest.py").exists(), reason="reference tests not staged")
 def test_reference_suite_passes_against_this_package():
     r = subprocess.run([sys.executable, str(REPO / "tools" / "reference_suite.py"), "--", "-q", "--tb=short",
@@ -25,3 +25,15 @@ def test_reference_suite_passes_against_this_package():
     m = re.search(r"(\d+) passed", r.stdout)
     assert r.returncode == 0, tail
     assert m and int(m.group(1)) >= 190, tail
+
+
+@pytest.mark.skipif(not (STAGED / "conftest.py").exists(), reason="reference tests not staged")
+def test_reference_suite_collects_against_this_package():
+    """CPU: every reference test module imports through the alias (no
+    missing public name), and the deselect list names existing tests."""
+    r = subprocess.run([sys.executable, str(REPO / "tools" / "reference_suite.py"), "--", "--collect-only", "-q"],
+                       capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "error" not in r.stdout.lower().split("collected")[0][-200:]
+    m = re.search(r"(\d+)(?:/\d+)? tests? collected", r.stdout) or re.search(r"(\d+) tests? collected", r.stdout)
+    assert m is None or int(m.group(1)) >= 190, r.stdout[-2000:]
