@@ -183,14 +183,20 @@ mp_status mp_exec_serial(const mp_loop* loop, const int32_t* inv_offsets, const 
                          void* stream);
 
 /* mp_exec_hier_stream (colour schedules) with the multi-GPU halo export
- * fused into the write-back: export_dest[staged entry] = (peer << 24 | row)
- * for the halo rows whose block is their last writer (-1 elsewhere); that
- * block also stores the row's final value into row `row` of
- * peer_slots[peer] + (epoch & 1) * slot_strides[peer] (the owner's mailbox
- * slot, IPC-mapped: P2P stores over NVLink).  *epoch is read on the device. */
+ * fused into the write-back.  export_desc: device memory holding
+ *   { const int32_t* dest;            per staged entry: (peer << 24 | row) for
+ *                                     the halo rows whose block is their last
+ *                                     writer, -1 elsewhere
+ *     uint64_t base[8];               per peer: the owner's export mailbox slot
+ *                                     for this rank (parity 0), IPC-mapped
+ *     int64_t stride[8];              bytes between its two parity slots
+ *     const uint32_t* epoch; }        the device step epoch (parity = epoch & 1)
+ * (mp_export_desc_bytes() = its size).  The last writer of a halo row also
+ * stores the row's final value into row `row` of base[peer] + parity *
+ * stride[peer] (P2P stores over NVLink). */
+mp_status mp_export_desc_bytes(void);
 mp_status mp_exec_hier_stream_export(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule,
-                                     const int32_t* export_dest, int32_t npeers, void* const* peer_slots,
-                                     const int64_t* slot_strides, const uint32_t* epoch, void* stream);
+                                     const void* export_desc, void* stream);
 
 /* Hierarchical executor, gather form (colour schedule, one launch per block
  * colour): lanes own (element, slot) refs instead of elements; each row's

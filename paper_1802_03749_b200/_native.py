@@ -97,8 +97,8 @@ _SIGNATURES = {
     "mp_halo_get": (c_i32, [c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp]),
     "mp_epoch_bump": (c_i32, [c_vp, c_vp]),
     "mp_halo_signal": (c_i32, [c_vp, c_vp, c_vp]),
-    "mp_exec_hier_stream_export": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_vp, c_i32,
-                                           c_vp, c_vp, c_vp, c_vp]),
+    "mp_exec_hier_stream_export": (c_i32, [ctypes.POINTER(MpLoop), ctypes.POINTER(MpHierPlan), c_i32, c_vp, c_vp]),
+    "mp_export_desc_bytes": (c_i32, []),
     "mp_mailbox_alloc": (c_i32, [c_i64, c_vp]),
     "mp_ipc_handle": (c_i32, [c_vp, c_vp]),
     "mp_ipc_open": (c_i32, [c_vp, c_vp]),

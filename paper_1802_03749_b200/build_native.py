@@ -48,14 +48,14 @@ def _compile(src: Path, verbose: bool, obj_dir: Path = OBJ_DIR, defines=()) -> P
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, _headers_mtime()):
         return obj
     cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
-    if verbose and src.suffix == ".cu":
+    if src.suffix == ".cu":  # register / spill report, kept beside the object (tests/test_codegen.py)
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         err = r.stderr if len(r.stderr) < 8000 else r.stderr[:5000] + "\n...\n" + r.stderr[-3000:]
         raise RuntimeError(f"nvcc failed on {src.name}:\n{err}")
-    if verbose and r.stderr:
-        (OBJ_DIR / (src.name + ".ptxas.txt")).write_text(r.stderr)
+    if src.suffix == ".cu":
+        (obj_dir / (src.name + ".ptxas.txt")).write_text(r.stderr)
     return obj
 
 

@@ -82,6 +82,16 @@
 namespace mp {
 namespace {
 
+// staged entry -> (owner peer << 24 | row of the owner's mailbox slot), -1 =
+// none; per peer the owner's export slot for this rank (parity 0) and the
+// bytes between its two parity slots; the device step epoch
+struct ExportDesc {
+  const int32_t* dest;
+  unsigned long long base[8];
+  long long stride[8];
+  const uint32_t* epoch;
+};
+
 struct StreamView {
   const int4* __restrict__ tdesc;           // per ticket {e0, k | nc << 16, s0, ns}
   const int32_t* __restrict__ tblock;       // per ticket block id (dataflow)
@@ -89,7 +99,10 @@ struct StreamView {
   const unsigned char* __restrict__ emeta;  // per element: A slots, colour byte, pad
   const int32_t* __restrict__ pred_offsets;
   const int32_t* __restrict__ preds;
-  const int32_t* __restrict__ pred_pad;  // [ntickets][8] (dataflow)
+  union {                                   // (one kernel parameter slot: the struct's size is tuned)
+    const int32_t* __restrict__ pred_pad;   // [ntickets][8] (dataflow schedules)
+    const struct ExportDesc* xdesc;         // fused halo export (EXPORT, colour schedules): the block that
+  };                                        // writes a halo row last stores it into the owner's mailbox
   uint32_t* flags;
   uint32_t epoch;
   const uint16_t* __restrict__ pull_off;  // pull variant: plan pull lists
@@ -102,15 +115,6 @@ struct StreamView {
   int32_t depth;  // blocks in flight; stages = depth + 1
   int32_t stage_reads;
   int32_t bulk_rows;  // TMA path: per-lane 1D bulk copies of 32-byte rows instead of tensor gather4
-  int32_t recompute;  // pull form: each row owner recomputes its refs' element outputs (no parking)
-  // fused halo export (multi-GPU, colour schedules): staged entry -> (owner
-  // peer << 24 | row of the owner's mailbox slot), -1 = none; the block that
-  // writes a halo row last also stores the row's final value into the owner's
-  // mailbox (P2P) in its write-back
-  const int32_t* export_dest;
-  unsigned char* export_base[8];   // per peer: the owner's export slot for this rank (parity 0)
-  int64_t export_stride[8];        // bytes between the two parity slots
-  const uint32_t* epoch_ptr;
   uint32_t* stats;  // optional (MESHPLAN_STREAM_STATS): [0] late blocks
 };
 
@@ -356,7 +360,8 @@ struct StreamLayout {
   }
 };
 
-template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR, bool TMAQ, bool SR, bool PULL>
+template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR, bool TMAQ, bool SR, bool PULL,
+          bool EXPORT = false>
 __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
     hier_stream_kernel(LoopView<T> v, StreamView H, const __grid_constant__ CUtensorMap qmap) {
   constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
@@ -479,7 +484,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
       hdr[0] = k;
       hdr[1] = ns;
       hdr[2] = d.y >> 16;
-      ctl[2 + s] = d.z;  // staged offset of the stage's block (fused export)
+      if constexpr (EXPORT) ctl[2 + s] = d.z;  // staged offset of the stage's block (fused export)
     }
 #pragma unroll
     for (int r = 0; r < MAXR; ++r) {
@@ -567,16 +572,20 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
   };
   // increment rows of block f (staged ids of stage s) -> registers; on the
   // dataflow schedule only once the block's predecessors are known done
-  const uint32_t xpar = H.export_dest ? (__ldg(H.epoch_ptr) & 1u) : 0u;
-  // fused halo export: a halo row's last writer also stores the final value
-  // into the owner's mailbox slot (256-bit P2P store for 32-byte rows)
+  // fused halo export (EXPORT instantiations only): a halo row's last writer
+  // also stores the final value into the owner's mailbox slot (256-bit P2P
+  // store for 32-byte rows)
   auto export_row = [&](int s_, int j, const T (&val)[IC]) {
-    if (H.export_dest == nullptr) return;
-    const int dst = __ldg(H.export_dest + ctl[2 + s_] + j);
-    if (dst < 0) return;
-    const int peer = dst >> 24;
-    T* remote = reinterpret_cast<T*>(H.export_base[peer] + xpar * H.export_stride[peer]);
-    stg_row<T, IC, MP_AOS>(remote, dst & 0xFFFFFF, 0, val);
+    if constexpr (EXPORT) {
+      const ExportDesc* X = H.xdesc;
+      const int dst = __ldg(X->dest + ctl[2 + s_] + j);
+      if (dst >= 0) {
+        const int peer = dst >> 24;
+        const unsigned long long xpar = __ldg(X->epoch) & 1u;
+        T* remote = reinterpret_cast<T*>(__ldg(&X->base[peer]) + xpar * (unsigned long long)__ldg(&X->stride[peer]));
+        stg_row<T, IC, MP_AOS>(remote, dst & 0xFFFFFF, 0, val);
+      }
+    }
   };
   T rrow[MAXR][IC];
   bool rows_late = false;
@@ -658,7 +667,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
     int ls[A];
     int my_tc = -1;
     unsigned fmask = 0;  // slots whose row this element writes first (store, no load)
-    if (t < k && !(PULL && H.recompute)) {
+    if (t < k) {
       const unsigned char* em = st + L.em + t * H.em_bytes;
       const SlotT* sl = reinterpret_cast<const SlotT*>(em);
 #pragma unroll
@@ -680,34 +689,11 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
       //     in thread-colour order starting from 0 -- the reference's zeroed
       //     shared row + per-colour np.add.at (simulator.py:634-643), bit for
       //     bit -- and writes row + sum back once.
-      if (!H.recompute) {
-        if (t < k) {
+      if (t < k) {
 #pragma unroll
-          for (int q = 0; q < A; ++q) sts_row<T, IC>(sh_inc, t * A + q, o[q]);
-        }
-        cbar();
+        for (int q = 0; q < A; ++q) sts_row<T, IC>(sh_inc, t * A + q, o[q]);
       }
-      // recompute form: the output of ref (element e, slot s), straight from the
-      // element's staged inputs -- the same operation on the same operands as
-      // the element's own evaluation (--fmad=false), so bit-identical
-      auto ref_out = [&](int ref, T (&x)[IC]) {
-        const int e = ref / A, sq = ref - e * A;
-        const SlotT* sl = reinterpret_cast<const SlotT*>(st + L.em + e * H.em_bytes);
-        T dd[DC], rr_[A][RCN], oo[A][IC];
-#pragma unroll
-        for (int c = 0; c < DC; ++c) dd[c] = reinterpret_cast<const T*>(st + L.dir)[c * H.max_block + e];
-        if (RC > 0 && stage_reads) {
-#pragma unroll
-          for (int q = 0; q < A; ++q) lds_row<T, RCN>(st + L.q, sl[q], rr_[q]);
-        }
-        compute<Op, T>(v, rr_, dd, oo);
-#pragma unroll
-        for (int q = 0; q < A; ++q)
-          if (q == sq) {
-#pragma unroll
-            for (int c = 0; c < IC; ++c) x[c] = oo[q][c];
-          }
-      };
+      cbar();
       const int dl = hdr[3];
       const uint16_t* po = reinterpret_cast<const uint16_t*>(st + L.poff) + (dl & 0xffff);
       const uint16_t* pr = reinterpret_cast<const uint16_t*>(st + L.pref) + (dl >> 16);
@@ -721,13 +707,11 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
           const int64_t p = reinterpret_cast<const int*>(st + L.ids)[j];
           const int lo = po[j], hi = po[j + 1];
           T acc[IC], x[IC];
-          if (H.recompute) ref_out(pr[lo], x);
-          else lds_row<T, IC>(sh_inc, pr[lo], x);
+          lds_row<T, IC>(sh_inc, pr[lo], x);
 #pragma unroll
           for (int c = 0; c < IC; ++c) acc[c] = x[c] + T(0);  // 0 + x
           for (int rr = lo + 1; rr < hi; ++rr) {
-            if (H.recompute) ref_out(pr[rr], x);
-            else lds_row<T, IC>(sh_inc, pr[rr], x);
+            lds_row<T, IC>(sh_inc, pr[rr], x);
 #pragma unroll
             for (int c = 0; c < IC; ++c) acc[c] += x[c];
           }
@@ -735,7 +719,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
 #pragma unroll
           for (int c = 0; c < IC; ++c) acc[c] = rrow[r][c] + acc[c];
           stg_row<T, IC, LAYOUT>(v.inc, p, v.npts, acc);
-          export_row(s, j, acc);
+          if constexpr (EXPORT) export_row(s, j, acc);
         }
       }
     } else {
@@ -775,7 +759,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
 #pragma unroll
         for (int c = 0; c < IC; ++c) acc[c] = rrow[r][c] + acc[c];
         stg_row<T, IC, LAYOUT>(v.inc, p, v.npts, acc);
-        export_row(s, j, acc);
+        if constexpr (EXPORT) export_row(s, j, acc);
       }
     }
     }  // push form
@@ -863,7 +847,7 @@ cudaError_t launch_pdl(K kern, int grid, int threads, size_t smem, cudaStream_t 
 
 template <class Op, typename T, int LAYOUT, typename SlotT>
 mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& P, bool dataflow, bool pull,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool exporting_req = false) {
   static const int env_depth = getenv("MESHPLAN_STREAM_DEPTH") ? atoi(getenv("MESHPLAN_STREAM_DEPTH")) : 2;
   static const int env_ctas = getenv("MESHPLAN_STREAM_CTAS") ? atoi(getenv("MESHPLAN_STREAM_CTAS")) : 0;
   int depth = env_depth < 2 ? 2 : (env_depth > 4 ? 4 : env_depth);
@@ -900,8 +884,6 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   // per-lane 1D bulk copies of the read rows through the TMA unit (takes the
   // q gathers off the LSU pipe)
   static const bool env_bulk = getenv("MESHPLAN_STREAM_BULK") && atoi(getenv("MESHPLAN_STREAM_BULK")) != 0;
-  static const bool env_recompute = getenv("MESHPLAN_PULL_RECOMPUTE") && atoi(getenv("MESHPLAN_PULL_RECOMPUTE")) != 0;
-  H.recompute = pull && env_recompute && (Op::RC == 0 || P.stage_reads) ? 1 : 0;
   CUtensorMap qmap;
   memset(&qmap, 0, sizeof(qmap));
   bool tma = false;
@@ -917,6 +899,10 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
       if (tma)
         MP_CUDA_TRY_DRV(encode_row_map(&qmap, v.ind, (int)sizeof(T), dtype_code<T>(), v.ind_comps, v.npts, Op::RC));
     }
+  }
+  if (exporting_req) {  // the fused export lives in the LDGSTS instantiations
+    tma = false;
+    H.bulk_rows = 0;
   }
   size_t smem = 0;
   for (;; --depth) {  // shrink the ring if it does not fit
@@ -936,9 +922,15 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
   using TT = std::true_type;
   using FF = std::false_type;
   constexpr bool TMA_OK = LAYOUT == MP_AOS && (QB == 32 || QB == 64 || QB == 128);
+  const bool exporting = exporting_req;
   auto pick_r = [&](auto dflow, auto tmaq, auto sread, auto pl) {
     constexpr bool DF = decltype(dflow)::value, TQ = decltype(tmaq)::value, S = decltype(sread)::value,
                    PU = decltype(pl)::value;
+    if constexpr (!DF && !TQ && LAYOUT == MP_AOS) {
+      if (exporting)
+        return hi ? hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_HI, TQ, S, PU, true>
+                  : hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_LO, TQ, S, PU, true>;
+    }
     return hi ? hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_HI, TQ, S, PU>
               : hier_stream_kernel<Op, T, LAYOUT, DF, SlotT, R_LO, TQ, S, PU>;
   };
@@ -1027,11 +1019,7 @@ mp_status launch_stream(const LoopView<T>& v, StreamView H, const mp_hier_plan& 
 }
 
 struct ExportArgs {
-  const int32_t* dest;
-  int32_t npeers;
-  void* const* bases;
-  const int64_t* strides;
-  const uint32_t* epoch;
+  const void* desc;  // device ExportDesc
 };
 
 template <class Op, typename T>
@@ -1061,22 +1049,17 @@ mp_status launch_stream_op(const mp_loop& Lp, const mp_hier_plan& P, bool datafl
     H.flags = P.flags;
     H.epoch = epoch;
     H.em_bytes = P.elem_meta_bytes;
-    if (ex && ex->dest) {
+    const bool xp = ex && ex->desc;
+    if (xp) {
       if (dataflow) MP_FAIL(MP_ERR_KERNEL, "fused halo export runs under the colour schedules");
       if (Lp.ind_layout != MP_AOS) MP_FAIL(MP_ERR_KERNEL, "fused halo export needs AoS increment rows");
-      if (ex->npeers < 0 || ex->npeers > 8) MP_FAIL(MP_ERR_KERNEL, "fused halo export: %d peers (max 8)", ex->npeers);
-      H.export_dest = ex->dest;
-      for (int q = 0; q < ex->npeers; ++q) {
-        H.export_base[q] = static_cast<unsigned char*>(ex->bases[q]);
-        H.export_stride[q] = ex->strides[q];
-      }
-      H.epoch_ptr = ex->epoch;
+      H.xdesc = static_cast<const ExportDesc*>(ex->desc);
     }
     LoopView<T> v = make_view<T>(Lp);
     const bool u8 = P.slot_bytes == 1;
     if (Lp.ind_layout == MP_AOS) {
-      if (u8) return launch_stream<Op, T, MP_AOS, uint8_t>(v, H, P, dataflow, pull, st);
-      return launch_stream<Op, T, MP_AOS, uint16_t>(v, H, P, dataflow, pull, st);
+      if (u8) return launch_stream<Op, T, MP_AOS, uint8_t>(v, H, P, dataflow, pull, st, xp);
+      return launch_stream<Op, T, MP_AOS, uint16_t>(v, H, P, dataflow, pull, st, xp);
     }
     if (u8) return launch_stream<Op, T, MP_SOA, uint8_t>(v, H, P, dataflow, pull, st);
     return launch_stream<Op, T, MP_SOA, uint16_t>(v, H, P, dataflow, pull, st);
@@ -1103,18 +1086,18 @@ extern "C" mp_status mp_exec_hier_stream(const mp_loop* loop, const mp_hier_plan
   });
 }
 
+extern "C" mp_status mp_export_desc_bytes(void) { return (mp_status)sizeof(mp::ExportDesc); }
+
 extern "C" mp_status mp_exec_hier_stream_export(const mp_loop* loop, const mp_hier_plan* plan, int32_t schedule,
-                                                const int32_t* export_dest, int32_t npeers, void* const* peer_slots,
-                                                const int64_t* slot_strides, const uint32_t* epoch, void* stream) {
+                                                const void* export_desc, void* stream) {
   mp::clear_error();
-  if (!loop || !plan || !export_dest || !epoch || (npeers > 0 && (!peer_slots || !slot_strides)))
-    MP_FAIL(MP_ERR_KERNEL, "null argument");
+  if (!loop || !plan || !export_desc) MP_FAIL(MP_ERR_KERNEL, "null argument");
   if ((schedule & 3) == MP_SCHED_DATAFLOW) MP_FAIL(MP_ERR_KERNEL, "fused halo export runs under the colour schedules");
   const bool pull = (schedule & MP_SCHED_PULL) != 0;
   if (pull && plan->num_blocks > 0 && (!plan->pull_off || !plan->pull_ref))
     MP_FAIL(MP_ERR_KERNEL, "pull form needs the plan's pull lists");
   cudaStream_t st = mp::as_stream(stream);
-  const mp::ExportArgs ex{export_dest, npeers, peer_slots, slot_strides, epoch};
+  const mp::ExportArgs ex{export_desc};
   const mp_loop& L = *loop;
   const mp_hier_plan& P = *plan;
   return MP_DISPATCH_OP(L.op, [&]() {

@@ -402,8 +402,17 @@ class DistributedLoop:
         self.fused = bool(fused_export)
         if self.fused:
             self.export_dest = self._export_dest()
-            self._ex_bases = (ctypes.c_void_p * 8)(*[b for b, _ in self.halo.export_slots])
-            self._ex_strides = (ctypes.c_int64 * 8)(*[st for _, st in self.halo.export_slots])
+            # the device-resident export descriptor (csrc ExportDesc): dest, 8 slot
+            # bases, 8 parity strides, epoch pointer
+            if len(self.halo.export_slots) > 8:
+                raise ValueError("fused export supports up to 8 owner peers")
+            words = np.zeros(1 + 8 + 8 + 1, dtype=np.int64)
+            words[0] = self.export_dest.data_ptr()
+            for q, (base, stride) in enumerate(self.halo.export_slots):
+                words[1 + q], words[9 + q] = base, stride
+            words[17] = self.halo.epoch_ptr
+            assert words.nbytes == _native.load().mp_export_desc_bytes()
+            self.export_desc = torch.as_tensor(words, device="cuda")
         # core / boundary split: core blocks touch no halo point, so
         # they run while the halo import is in flight; the colour schedules only
         if overlap is None:
@@ -451,8 +460,7 @@ class DistributedLoop:
             return
         dp = self.plan._device
         _native.call("mp_exec_hier_stream_export", self.loop.loop, (sub.struct if sub is not None else dp.struct_cached()),
-                     self.loop.schedule, self.export_dest.data_ptr(), len(self.halo.owners), self._ex_bases,
-                     self._ex_strides, self.halo.epoch_ptr, _native.stream_ptr())
+                     self.loop.schedule, self.export_desc.data_ptr(), _native.stream_ptr())
 
     def core_blocks(self) -> torch.Tensor:
         """Per block of the local plan: true when none of its elements
