@@ -75,6 +75,9 @@
 #ifndef MP_STREAM_MAXREG
 #define MP_STREAM_MAXREG 72  // 7 CTAs of 128 threads per SM
 #endif
+#ifndef MP_STREAM_MAXREG_EXPORT
+#define MP_STREAM_MAXREG_EXPORT 72  // fused halo export: 7 CTAs/SM (24 bytes of spill; C5 at world size 1: 1.296 vs 1.295 ms without the export)
+#endif
 #ifndef MP_STREAM_MAXREG_DF
 #define MP_STREAM_MAXREG_DF 72  // dataflow: 128 + 32 threads, 5 CTAs/SM (64 spills on the critical path)
 #endif
@@ -362,7 +365,7 @@ struct StreamLayout {
 
 template <class Op, typename T, int LAYOUT, bool DATAFLOW, typename SlotT, int MAXR, bool TMAQ, bool SR, bool PULL,
           bool EXPORT = false>
-__global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
+__global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : (EXPORT ? MP_STREAM_MAXREG_EXPORT : MP_STREAM_MAXREG))
     hier_stream_kernel(LoopView<T> v, StreamView H, const __grid_constant__ CUtensorMap qmap) {
   constexpr int A = Op::ARITY, RC = Op::RC, IC = Op::IC, DC = Op::DC, RCN = RcArr<Op>::N;
   using L_t = StreamLayout<Op, T>;
@@ -572,19 +575,25 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
   };
   // increment rows of block f (staged ids of stage s) -> registers; on the
   // dataflow schedule only once the block's predecessors are known done
-  // fused halo export (EXPORT instantiations only): a halo row's last writer
-  // also stores the final value into the owner's mailbox slot (256-bit P2P
-  // store for 32-byte rows)
-  auto export_row = [&](int s_, int j, const T (&val)[IC]) {
+  // fused halo export (EXPORT instantiations only): the block that writes a
+  // halo row last stores the row's final value into the owner's mailbox slot
+  // instead of the local row (which is re-zeroed after the step and never
+  // read again): one 256-bit P2P store in place of the local one
+  auto write_row = [&](int s_, int j, int64_t p, const T (&val)[IC]) {
     if constexpr (EXPORT) {
       const ExportDesc* X = H.xdesc;
       const int dst = __ldg(X->dest + ctl[2 + s_] + j);
+      T* base = v.inc;
+      int64_t row = p;
       if (dst >= 0) {
         const int peer = dst >> 24;
-        const unsigned long long xpar = __ldg(X->epoch) & 1u;
-        T* remote = reinterpret_cast<T*>(__ldg(&X->base[peer]) + xpar * (unsigned long long)__ldg(&X->stride[peer]));
-        stg_row<T, IC, MP_AOS>(remote, dst & 0xFFFFFF, 0, val);
+        base = reinterpret_cast<T*>(__ldg(&X->base[peer]) +
+                                    (unsigned long long)(__ldg(X->epoch) & 1u) * (unsigned long long)__ldg(&X->stride[peer]));
+        row = dst & 0xFFFFFF;
       }
+      stg_row<T, IC, MP_AOS>(base, row, 0, val);
+    } else {
+      stg_row<T, IC, LAYOUT>(v.inc, p, v.npts, val);
     }
   };
   T rrow[MAXR][IC];
@@ -718,8 +727,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
           if (DATAFLOW && rows_late) ldg_row<T, IC, LAYOUT>(v.inc, p, v.npts, true, rrow[r]);
 #pragma unroll
           for (int c = 0; c < IC; ++c) acc[c] = rrow[r][c] + acc[c];
-          stg_row<T, IC, LAYOUT>(v.inc, p, v.npts, acc);
-          if constexpr (EXPORT) export_row(s, j, acc);
+          write_row(s, j, p, acc);
         }
       }
     } else {
@@ -758,8 +766,7 @@ __global__ void __maxnreg__(DATAFLOW ? MP_STREAM_MAXREG_DF : MP_STREAM_MAXREG)
         if (DATAFLOW && rows_late) ldg_row<T, IC, LAYOUT>(v.inc, p, v.npts, true, rrow[r]);
 #pragma unroll
         for (int c = 0; c < IC; ++c) acc[c] = rrow[r][c] + acc[c];
-        stg_row<T, IC, LAYOUT>(v.inc, p, v.npts, acc);
-        if constexpr (EXPORT) export_row(s, j, acc);
+        write_row(s, j, p, acc);
       }
     }
     }  // push form
