@@ -26,6 +26,7 @@ otherwise.
 
 import ctypes
 import queue
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -205,11 +206,14 @@ class HaloExchange:
 
 
 class PeerHub:
-    """Mailbox registry of ranks running as threads of one process (one device
-    or several): a mailbox is published as its raw device pointer."""
+    """Mailbox registry of ranks running as threads of one process, each on its
+    own device: a mailbox is published as its raw device pointer.  (Ranks
+    sharing one device must be processes -- ``ipc_connector``: threads share
+    the process's hardware work queues, where one rank's waiting ``get`` can
+    hold up another rank's ``put``.)"""
 
     def __init__(self):
-        self._boxes, self._cv = {}, __import__("threading").Condition()
+        self._boxes, self._cv = {}, threading.Condition()
 
     def connector(self, rank: int):
         def publish(ptr: int, layout: dict, needed) -> dict:
@@ -255,8 +259,11 @@ class PeerExchange:
     (``mp_halo_put``: P2P stores, then a release of the epoch in the peer's
     flag) and waits for / unpacks its own halo rows (``mp_halo_get``);
     ``export_increments`` does the same for halo increments (added by the
-    owner) and re-zeroes the halo rows.  Nothing waits on the host, so a whole
-    step is capturable as a CUDA graph (``DistributedLoop.capture``).
+    owner) and re-zeroes the halo rows -- or, with ``fused_export``, only
+    releases the epoch (``mp_halo_signal``): the loop's write-back has already
+    stored the rows into the owners' slots (``export_slots``).  Nothing waits
+    on the host, so a whole step is capturable as a CUDA graph
+    (``DistributedLoop.capture``).
     ``publish(ptr, layout, needed)`` exchanges mailboxes (``PeerHub`` for
     threads, ``ipc_connector`` for processes)."""
 
