@@ -14,15 +14,23 @@ from pathlib import Path
 LIB = Path(__file__).resolve().parents[1] / "paper_1802_03749_b200" / "lib" / "libmeshplan_b200.so"
 # (label, demangled-name fragments that must all appear)
 KERNELS = [
-    ("C5 headline: hier_stream_kernel<OpFlux, double, AoS, colour, u8 slots>",
-     ["hier_stream_kernel", "OpFlux", "Ed", "Li0ELb0EhLi2ELb0ELb1ELb0E"]),
-    ("C5 pull form: hier_stream_kernel<OpFlux, double, ..., PULL>", ["hier_stream_kernel", "OpFlux", "Ed", "Li0ELb0EhLi2ELb0ELb1ELb1E"]),
+    ("C5 / C1 headline: hier_stream_kernel<OpFlux, double, AoS, colour, u8 slots, push>",
+     ["hier_stream_kernel", "OpFluxEdLi0ELb0EhLi2ELb0ELb1ELb0ELb0EEEv"]),
+    ("C5 pull form: hier_stream_kernel<OpFlux, double, ..., PULL>", ["hier_stream_kernel", "OpFluxEdLi0ELb0EhLi2ELb0ELb1ELb1ELb0EEEv"]),
+    ("multi-GPU fused export: hier_stream_kernel<OpFlux, double, ..., push, EXPORT>",
+     ["hier_stream_kernel", "OpFluxEdLi0ELb0EhLi2ELb0ELb1ELb0ELb1EEEv"]),
+    ("C2 headline: hier_stream_kernel<OpFlux, float, AoS, colour, u8 slots, push>",
+     ["hier_stream_kernel", "OpFluxEfLi0ELb0EhLi2ELb0ELb1ELb0ELb0EEEv"]),
+    ("C3 headline: hier_stream_kernel<OpScatter8, double, AoS, colour, u16 slots, 4 rows/thread>",
+     ["hier_stream_kernel", "OpScatter8EdLi0ELb0EtLi4E"]),
+    ("gather form: hier_gather_kernel<OpFlux, double>", ["hier_gather_kernel", "OpFluxEdh"]),
     ("C4 headline: hier_pipe_kernel<OpFaceFlux, double, AoS, colour, pull>",
      ["hier_pipe_kernel", "OpFaceFluxEdLi0ELb0E", "Lb1EEEv"]),
     ("global colouring baseline: global_colour_kernel<OpFlux, double>", ["global_colour_kernel", "OpFlux", "Ed"]),
     ("atomics baseline: atomic_kernel<OpFlux, double>", ["atomic_kernel", "OpFlux", "Ed"]),
     ("block colouring: greedy_blocks_kernel<2>", ["greedy_blocks_kernel", "ILi2E"]),
     ("halo put (peer memory): halo_put_kernel<double>", ["halo_put_kernel", "IdE"]),
+    ("halo get (peer memory): halo_get_kernel<double>", ["halo_get_kernel", "IdE"]),
 ]
 CLASSES = {"LDGSTS": "cp.async gather", "UTMALDG": "TMA tensor load", "UBLKCP": "TMA bulk copy", "LDS": "shared load",
            "STS": "shared store", "LDG": "global load", "STG": "global store", "BAR": "barrier", "RED": "reduction",
