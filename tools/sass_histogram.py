@@ -64,16 +64,20 @@ def main():
             continue
         name, body = min(hits, key=lambda nb: len(nb[0]))
         ops = collections.Counter()
+        wide = collections.Counter()  # 256-bit global accesses (LDG/STG.E.ENL2.256)
         for line in body:
             m = re.search(r"/\*[0-9a-f]{4,}\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_]*)(\.[A-Z0-9_.]+)?", line)
             if m:
                 ops[m.group(1)] += 1
+                if m.group(2) and "ENL2.256" in m.group(2):
+                    wide[m.group(1)] += 1
         total = sum(ops.values())
         print(f"## {label}\n\n`{name[:160]}`\n\n{total} instructions.  Data movement / sync:\n")
         print("| opcode | what | count |\n|---|---|---|")
         for op in sorted(ops, key=lambda o: -ops[o]):
             if op in CLASSES:
-                print(f"| {op} | {CLASSES[op]} | {ops[op]} |")
+                extra = f" ({wide[op]} of them 256-bit `.ENL2.256`)" if wide[op] else ""
+                print(f"| {op} | {CLASSES[op]} | {ops[op]}{extra} |")
         others = ", ".join(f"{o} {c}" for o, c in ops.most_common(12) if o not in CLASSES)
         print(f"\nMost frequent others: {others}\n")
 
