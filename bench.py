@@ -385,6 +385,22 @@ def verify_full(hier, glob, kernel, main, gl):
             "nonzero_rows": int(np.count_nonzero(np.any(want != 0, axis=1)))}
 
 
+def reference_plan_times(args):
+    """The reference planner's wall time for the same plans (next
+    to the GPU plan-build times), as recorded by tests/golden/make_fingerprints.py
+    when it ran the real reference at these sizes (8-core build container,
+    numba backend); None where it was not run."""
+    try:
+        fp = json.loads((REPO / "tests" / "golden" / "fingerprints.json").read_text())
+    except (OSError, ValueError):
+        return None
+    name = args.config if args.block_size == 128 else f"{args.config}k{args.block_size}"
+    plans = fp.get(name, {}).get("plans", {})
+    out = {k: v.get("build_s") for k, v in plans.items()
+           if k in (f"hier/{args.reorder}", f"global/{args.global_reorder}")}
+    return out or None
+
+
 def our_arm(args):
     import torch
 
@@ -583,7 +599,8 @@ def our_arm(args):
         "gpu_launches": int(launches * args.steps),
         "clocks": clocks,
         "cpu_baseline": cpu,
-        "plan_build_s": {"generate": round(t_gen, 2), "hier": round(t_plan_h, 2), "global": round(t_plan_g, 2)},
+        "plan_build_s": {"generate": round(t_gen, 2), "hier": round(t_plan_h, 2), "global": round(t_plan_g, 2),
+                         "reference": reference_plan_times(args)},
     }
     print(json.dumps(line), flush=True)
     return 0
