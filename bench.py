@@ -47,10 +47,14 @@ DEFAULT_REORDER = {"C1": "gps", "C2": "gps", "C3": "none", "C4": "partition", "C
 #: 1.02 vs 1.08 ms, tools/gpu_c4bs.sh), 128 elsewhere
 DEFAULT_BLOCK = {"C4": 256}
 #: other block layouts timed beside the headline (reported as vs_layout):
-#: name -> (reorder, block size or None for --block-size, schedule(s) or None for the headline's)
+#: name -> (reorder, block size or None for --block-size, schedule(s) or None
+#: for the headline's[, indirect-data layout, default --layout])
 COMPARE_REORDER = {"C2": (("none", None, None),),
-                   # the paper's handcrafted hex blocks (shape from tools/shape_sweep.sh)
-                   "C4": (("structured:4,4,8", 480, ("stream-pull", "pipelined", "pipelined-pull", "stream")),)}
+                   # the paper's handcrafted hex blocks (shape from tools/shape_sweep.sh),
+                   # in AoS and in SoA (each consumed state / flux component a contiguous plane:
+                   # 0.86 vs 0.93 ms, profiles/r02/c4_soa.log)
+                   "C4": (("structured:4,4,8", 480, ("stream-pull", "pipelined", "pipelined-pull", "stream")),
+                          ("structured:4,4,8", 480, ("stream-pull", "stream"), "soa"))}
 CONFIGS = {
     # name: (family, dims, kernel, dtype, staging)
     "C1": ("quad2d", (848, 848), "flux", "f64", "all-indirect"),
@@ -465,12 +469,13 @@ def our_arm(args):
     # the configs that compare block layouts (BASELINE.json configs[1]: natural
     # vs GPS-reordered) time the other layout with the headline schedule too
     vs_layout = {}
-    for other, bs, sched in COMPARE_REORDER.get(args.config, ()):
-        if other == args.reorder:
+    for other, bs, sched, *lay in COMPARE_REORDER.get(args.config, ()):
+        lay = lay[0] if lay else args.layout
+        if other == args.reorder and lay == args.layout:
             continue
         t0 = time.perf_counter()
         alt = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(
-            reorder=other, layout=args.layout, staging=staging, block_size=bs or args.block_size))
+            reorder=other, layout=lay, staging=staging, block_size=bs or args.block_size))
         t_alt = time.perf_counter() - t0
         by_sched = {}
         for sc in (sched if isinstance(sched, tuple) else (sched or args.schedule,)):
@@ -479,10 +484,10 @@ def our_arm(args):
             del alt_loop
         sc = min(by_sched, key=by_sched.get)
         ms_alt = by_sched[sc]
-        vs_layout[other] = {"ms_per_step": round(ms_alt, 5), "gbps": round(ub / (ms_alt * 1e-3) / 1e9, 2),
+        vs_layout[other if lay == args.layout else f"{other}/{lay}"] = {"ms_per_step": round(ms_alt, 5), "gbps": round(ub / (ms_alt * 1e-3) / 1e9, 2),
                             "frac": round(cb / (ms_alt * 1e-3) / 1e9 / hbm_peak()[0], 4),
                             "frac_formula": round(ub / (ms_alt * 1e-3) / 1e9 / hbm_peak()[0], 4),
-                            "block_size": bs or args.block_size, "schedule": sc,
+                            "block_size": bs or args.block_size, "schedule": sc, "layout": lay,
                             "ms_by_schedule": {k: round(v, 5) for k, v in by_sched.items()},
                             "reuse_factor": round(mp.reuse_factor(alt), 4),
                             "block_colours": alt.block_colours.num_colours, "plan_build_s": round(t_alt, 2)}
