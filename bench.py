@@ -46,10 +46,16 @@ DEFAULT_REORDER = {"C1": "gps", "C2": "gps", "C3": "none", "C4": "partition", "C
 #: the face loop at 256 faces (reuse 3.22 vs 2.92 at 128; pipelined-pull
 #: 1.02 vs 1.08 ms, tools/gpu_c4bs.sh), 128 elsewhere
 DEFAULT_BLOCK = {"C4": 256}
+#: element orders of the global-colouring baseline timed beside the default
+#: (GPS) one (global/none as well); the speed-up is also quoted
+#: over the faster of the two
+GLOBAL_COMPARE = {c: ("none",) for c in ("C1", "C2", "C3", "C4", "C5")}
 #: other block layouts timed beside the headline (reported as vs_layout):
 #: name -> (reorder, block size or None for --block-size, schedule(s) or None
 #: for the headline's[, indirect-data layout, default --layout])
-COMPARE_REORDER = {"C2": (("none", None, None),),
+COMPARE_REORDER = {"C1": (("none", None, None), ("partition", None, None),  # hier/{none,gps,partition}
+                          ("gps", 448, None), ("gps", 480, None)),                # and the paper's 448/480-element blocks
+                   "C2": (("none", None, None),),
                    # the paper's handcrafted hex blocks (shape from tools/shape_sweep.sh),
                    # in AoS and in SoA (each consumed state / flux component a contiguous plane:
                    # 0.86 vs 0.93 ms, profiles/r02/c4_soa.log)
@@ -469,9 +475,18 @@ def our_arm(args):
     # the configs that compare block layouts (BASELINE.json configs[1]: natural
     # vs GPS-reordered) time the other layout with the headline schedule too
     vs_layout = {}
+    global_by_reorder = {}
+    for other in GLOBAL_COMPARE.get(args.config, ()):
+        if other == args.global_reorder:
+            continue
+        g_alt = mp.build_global_plan(mesh, kernel, mp.PlanConfig(strategy="global", reorder=other, layout=args.layout,
+                                                                   block_size=args.block_size))
+        ms_g = statistics.median(time_steps(mp.bind(g_alt, kernel).run, args.steps, args.warmup, flush))
+        global_by_reorder[other] = {"ms_per_step": round(ms_g, 5), "colours": g_alt.num_colours}
+        del g_alt
     for other, bs, sched, *lay in COMPARE_REORDER.get(args.config, ()):
         lay = lay[0] if lay else args.layout
-        if other == args.reorder and lay == args.layout:
+        if other == args.reorder and lay == args.layout and (bs or args.block_size) == args.block_size:
             continue
         t0 = time.perf_counter()
         alt = mp.build_hierarchical_plan(mesh, kernel, mp.PlanConfig(
@@ -484,7 +499,8 @@ def our_arm(args):
             del alt_loop
         sc = min(by_sched, key=by_sched.get)
         ms_alt = by_sched[sc]
-        vs_layout[other if lay == args.layout else f"{other}/{lay}"] = {"ms_per_step": round(ms_alt, 5), "gbps": round(ub / (ms_alt * 1e-3) / 1e9, 2),
+        key = other + ("" if lay == args.layout else f"/{lay}") + (f"@{bs}" if bs and other == args.reorder else "")
+        vs_layout[key] = {"ms_per_step": round(ms_alt, 5), "gbps": round(ub / (ms_alt * 1e-3) / 1e9, 2),
                             "frac": round(cb / (ms_alt * 1e-3) / 1e9 / hbm_peak()[0], 4),
                             "frac_formula": round(ub / (ms_alt * 1e-3) / 1e9 / hbm_peak()[0], 4),
                             "block_size": bs or args.block_size, "schedule": sc, "layout": lay,
@@ -566,6 +582,8 @@ def our_arm(args):
         "vs_global": {
             "global_ms": round(ms_glob, 5), "global_gbps": round(ub / (ms_glob * 1e-3) / 1e9, 2),
             "global_reorder": args.global_reorder, "global_colours": glob.num_colours,
+            "global_other_orders": global_by_reorder or None,
+            "speedup_hier_over_best_global": round(min([ms_glob] + [v["ms_per_step"] for v in global_by_reorder.values()]) / ms, 3),
             "hier_ms_by_schedule": per_schedule,
             "headline_direct_ms": round(ms_direct, 5),
             "headline_graph_ms": None if ms_graph is None else round(ms_graph, 5),
