@@ -17,9 +17,12 @@ equal the formula's, C4's are 1,915 MB of the formula's 3,387 MB);
 effective GB/s.  One step = one full execution of the loop over
 the mesh.  Effective GB/s uses the paper's formula (simulator.py:315-328):
 each array once, the incremented array twice, 4-byte mapping entries.
-With N>1 GPUs the mesh is decomposed into x-slabs (owner compute, NCCL halo
-exchange of q and of increments); `value` is the whole-mesh bytes over the
-max-over-ranks step time (strong scaling: the mesh is fixed).
+With N>1 GPUs the mesh is decomposed into x-slabs (owner compute; halo
+import of q and export of increments through peer memory -- CUDA IPC
+mailboxes, the export fused into the boundary blocks' write-back, each step
+one CUDA graph; NCCL send/recv with --transport nccl); `value` is the
+whole-mesh bytes over the max-over-ranks step time (strong scaling: the mesh
+is fixed).
 """
 
 import argparse
