@@ -29,6 +29,9 @@
 // is capped at the occupancy-derived resident count).
 #include <stdlib.h>
 
+#include <mutex>
+#include <vector>
+
 #include "mp_loop.cuh"
 
 namespace mp {
@@ -528,31 +531,100 @@ __global__ void __launch_bounds__(1024) hier_pipe_kernel(LoopView<T> v, PipeView
   }
 }
 
+// resident CTAs per SM for (kernel, threads, shared bytes) on the current
+// device, cached process-wide (the query costs microseconds per call); raises
+// the kernel's dynamic shared-memory limit first
+cudaError_t pipe_occupancy(const void* kern, int threads, size_t smem, int* occ) {
+  struct Entry {
+    const void* k;
+    int threads, dev;
+    size_t smem;
+    int occ;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& c : cache)
+      if (c.k == kern && c.threads == threads && c.dev == dev && c.smem == smem) {
+        *occ = c.occ;
+        return cudaSuccess;
+      }
+  }
+  e = raise_smem_limit(kern, smem);
+  if (e) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, threads, smem);
+  if (e) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  cache.push_back({kern, threads, dev, smem, *occ});
+  return cudaSuccess;
+}
+
 template <class Op, typename T, int LAYOUT, typename SlotT, bool PULL>
 mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, bool dataflow, cudaStream_t st) {
   const StageLayout<Op, T, SlotT> L(P.max_staged, P.block_size, P.stage_reads != 0);
   const bool map_rows = Op::RC > 0 && !P.stage_reads;
   const size_t ring = (size_t)(PIPE_K + 1) * (((P.max_staged + 11) & ~3) * 4 +
                                               (map_rows ? (size_t)P.block_size * Op::ARITY * 4 : 0));
-  static const int env_stages = getenv("MESHPLAN_PIPE_STAGES") ? atoi(getenv("MESHPLAN_PIPE_STAGES")) : 3;
+  static const int env_stages = getenv("MESHPLAN_PIPE_STAGES") ? atoi(getenv("MESHPLAN_PIPE_STAGES")) : 0;
   static const int env_ctas = getenv("MESHPLAN_PIPE_CTAS") ? atoi(getenv("MESHPLAN_PIPE_CTAS")) : 0;
-  const int NSTAGE = env_stages < 2 ? 2 : (env_stages > MAX_STAGES ? MAX_STAGES : env_stages);
-  H.nstage = NSTAGE;
-  const size_t smem =
-      128 + inc_buffer_bytes<Op, T, PULL>(P.max_staged, P.block_size) + (size_t)NSTAGE * L.bytes + ring;
-  if (smem > 227 * 1024)
-    MP_FAIL(MP_ERR_CAPACITY, "pipelined stages need %zu shared bytes, over the 232448-byte limit", smem);
+  // shared bytes per SM the resident CTAs may take: the rest stays L1 data
+  // cache (on the face loop, above ~200 KB per SM every plan measured ~25 %
+  // slower: C4 k-way pull 1.28 vs 1.02 ms, 4x4x8 pull 0.99 vs 0.83 ms, k-way
+  // push 1.30 vs 1.03 ms, profiles/r02/pipe_stages.log, pipe_auto.log)
+  static const int env_budget = getenv("MESHPLAN_PIPE_SMEM_KB") ? atoi(getenv("MESHPLAN_PIPE_SMEM_KB")) : 192;
   const int consumers = ((P.block_size + 31) / 32) * 32;
   const int threads = consumers + 32;
   auto kern = dataflow ? hier_pipe_kernel<Op, T, LAYOUT, true, SlotT, PULL>
                        : hier_pipe_kernel<Op, T, LAYOUT, false, SlotT, PULL>;
-  MP_CUDA_TRY(raise_smem_limit(reinterpret_cast<const void*>(kern), smem));
-  int per_sm = 0, dev = 0, sms = 0;
-  MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  auto smem_of = [&](int ns) {
+    return 128 + inc_buffer_bytes<Op, T, PULL>(P.max_staged, P.block_size) + (size_t)ns * L.bytes + ring;
+  };
+  // ring depth and CTAs per SM: the most CTAs that fit the budget (and the
+  // occupancy limit), then the deepest ring at that count (2..4 stages)
+  int NSTAGE = 0, per_sm = 0, occ2 = 0;
+  for (int ns = 2; ns <= 4; ++ns) {
+    if (env_stages && ns != (env_stages < 2 ? 2 : (env_stages > MAX_STAGES ? MAX_STAGES : env_stages))) continue;
+    const size_t sm = smem_of(ns);
+    if (sm > 227 * 1024) break;
+    int occ = 0;
+    MP_CUDA_TRY(pipe_occupancy(reinterpret_cast<const void*>(kern), threads, sm, &occ));
+    if (ns == 2) occ2 = occ;
+    int cap = (int)(((size_t)env_budget * 1024) / (sm + 1024));
+    if (env_stages || cap < 1) cap = occ;  // an explicit ring depth keeps the occupancy limit
+    if (cap > occ) cap = occ;
+    if (cap >= 1 && (NSTAGE == 0 || cap >= per_sm)) {
+      NSTAGE = ns;
+      per_sm = cap;
+    }
+  }
+  if (!env_stages && per_sm < 2 && occ2 >= 2) {  // never one CTA per SM where two fit: two stages, two CTAs
+    NSTAGE = 2;
+    per_sm = 2;
+  }
+  if (env_stages > 4) {  // deeper rings on request
+    NSTAGE = env_stages > MAX_STAGES ? MAX_STAGES : env_stages;
+    MP_CUDA_TRY(pipe_occupancy(reinterpret_cast<const void*>(kern), threads, smem_of(NSTAGE), &per_sm));
+  }
+  if (NSTAGE == 0) MP_FAIL(MP_ERR_CAPACITY, "pipelined stages need %zu shared bytes, over the 232448-byte limit", smem_of(2));
+  const size_t smem = smem_of(NSTAGE);
+  H.nstage = NSTAGE;
+  int dev = 0, sms = 0;
   MP_CUDA_TRY(cudaGetDevice(&dev));
   MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (per_sm < 1) MP_FAIL(MP_ERR_CAPACITY, "pipelined executor does not fit on an SM (%zu shared bytes)", smem);
   if (env_ctas > 0 && env_ctas < per_sm) per_sm = env_ctas;
+  {  // shared-memory carve-out for exactly the resident CTAs (the rest is L1)
+    const int pct = (int)((100 * (size_t)per_sm * (smem + 1024) + 227 * 1024 - 1) / (228 * 1024));
+    MP_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     pct > 100 ? 100 : pct));
+  }
+  if (getenv("MESHPLAN_PIPE_VERBOSE"))
+    fprintf(stderr, "[pipe] pull=%d stages=%d stage_bytes=%d smem=%zu threads=%d per_sm=%d\n", (int)PULL, NSTAGE,
+            (int)L.bytes, smem, threads, per_sm);
   const int resident = per_sm * sms;
   if (dataflow) {
     H.list = P.order;
