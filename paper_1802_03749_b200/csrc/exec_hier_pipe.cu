@@ -617,7 +617,8 @@ mp_status launch_pipe(const LoopView<T>& v, PipeView H, const mp_hier_plan& P, b
   MP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (per_sm < 1) MP_FAIL(MP_ERR_CAPACITY, "pipelined executor does not fit on an SM (%zu shared bytes)", smem);
   if (env_ctas > 0 && env_ctas < per_sm) per_sm = env_ctas;
-  {  // shared-memory carve-out for exactly the resident CTAs (the rest is L1)
+  if (!dataflow) {  // shared-memory carve-out for exactly the resident CTAs (the rest is L1); the
+                    // static-claim dataflow grid keeps the default, which holds every CTA it counts on
     const int pct = (int)((100 * (size_t)per_sm * (smem + 1024) + 227 * 1024 - 1) / (228 * 1024));
     MP_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributePreferredSharedMemoryCarveout,
                                      pct > 100 ? 100 : pct));
