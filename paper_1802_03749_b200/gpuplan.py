@@ -33,7 +33,7 @@ import torch
 
 from . import _native
 from .errors import CapacityError, KernelSpecError, MeshValidationError
-from .mesh import DataArray, Mapping, Mesh
+from .mesh import Mapping, Mesh
 
 DEV = "cuda"
 
